@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""bench.py -- PBN trajectory throughput on B200 (BASELINE.json metric).
+
+A "step" is one pass of the whole hot path over one
+batch of synthetic input: pbn_simulate on config C4 (n=2000, 16384 chains,
+5e4 burn-in + 5e4 recorded transitions per chain, fused indicator /
+transition / batch (kappa=500) counters, packed indicator bits, totals).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C4] [--chains N] [--burn-in B] [--window S]
+
+Under torchrun (N > 1) every rank runs the same per-GPU workload on its own
+chain range (weak scaling, no data-path collective); the max over ranks of
+the device-timed region is used.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from workloads import CONFIGS, config_model, config_predicate  # noqa: E402
+
+METRIC = "PBN node-updates/sec and chain-steps/sec on 1 B200; fraction of int/smem roofline"
+UNIT = "node-updates/s"
+SM_COUNT_B200 = 148
+ALU_LANES_PER_CLK_PER_SM = 64   # ALU pipe: rt_SMSP = 2 cycles per warp-instruction (B300_MICROARCH.md)
+
+
+def algorithmic_alu_ops(model) -> float:
+    """ALU-pipe integer ops per node-update the method needs:
+    RNG 1/4 Philox4x32-10 = 5 LOP3 (the 5 IMAD.WIDE go to the FMA pipe);
+    decide 1 + (ell-1) compares; gather 2 per selected parent; lookup 2
+    (+1 word select when theta >= 6); commit 1."""
+    ell = np.diff(model.fn_off).astype(np.float64)
+    theta = np.diff(model.par_off).astype(np.float64)
+    # expected over the selected function: selection probabilities weight theta
+    node_of_fn = np.repeat(np.arange(model.n), np.diff(model.fn_off))
+    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n)
+    sel_big = np.bincount(node_of_fn, weights=model.sel_prob * (theta >= 6), minlength=model.n)
+    return float(5.0 + ell.mean() + 2.0 * sel_theta.mean() + 2.0 + sel_big.mean() + 1.0)
+
+
+# --------------------------------------------------------------------------
+# clocks during the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference) -- the only
+# places bench.py executes oracle/.
+# --------------------------------------------------------------------------
+def oracle_sample(model, pred, seed: int, chains: int, steps: int, threads: int) -> tuple[float, dict]:
+    from oracle import sim as osim
+    from oracle import stats as ostats
+    t0 = time.perf_counter()
+    _, I = osim.simulate(model, pred, seed=seed, chain_ids=np.arange(chains), step0=0, burn_in=0,
+                         steps=steps, threads=threads)
+    _ = [ostats.window_stats(I[c], 500) for c in range(chains)]
+    dt = time.perf_counter() - t0
+    nu = chains * steps * model.n
+    return nu / dt, {"chains": chains, "steps_per_chain": steps, "seconds": dt, "node_updates": nu}
+
+
+def run_reference(args, cfg, model, pred, rank: int):
+    if rank != 0:
+        return
+    cores = ncores()
+    chains = cores
+    steps = max(200, int(args.ref_steps))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, info = oracle_sample(model, pred, cfg.sim_seed, chains, steps, cores)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    sample = (f"{chains} chains x {steps} transitions of {cfg.key} (n={model.n}) per step, "
+              f"oracle C simulator + window statistics, {cores} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": chains * steps * model.n / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(args, cfg, model),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, cfg, model) -> dict:
+    return {
+        "workload": f"{cfg.key}: n={model.n} PBN, ell~U{{{cfg.ell[0]}..{cfg.ell[1]}}}, "
+                    f"theta~U{{{cfg.theta[0]}..{cfg.theta[1]}}}, p={cfg.p}, "
+                    f"{args.chains} chains x ({args.burn_in} burn-in + {args.window} recorded) "
+                    f"transitions, fused c1/n01/n10/first-last, batch kappa={cfg.batch}, bits, totals",
+        "chains_per_gpu": args.chains, "burn_in": args.burn_in, "window": args.window,
+        "batch": cfg.batch, "n": model.n, "functions": int(model.nf),
+        "density": float(model.par_off[-1]) / model.n, "seed": cfg.sim_seed,
+        "semantics": "VECTOR", "l2": "256 MiB buffer written between timed steps",
+    }
+
+
+# --------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--chains", type=int, default=None)
+    ap.add_argument("--burn-in", type=int, default=None)
+    ap.add_argument("--window", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=2500)
+    ap.add_argument("--groups", type=int, default=0)
+    ap.add_argument("--warps", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
+
+    cfg = CONFIGS[args.config]
+    args.chains = args.chains or cfg.chains
+    args.burn_in = cfg.burn_in if args.burn_in is None else args.burn_in
+    args.window = cfg.steps if args.window is None else args.window
+    model, pred = config_model(args.config), config_predicate(args.config)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, model, pred, rank)
+        return
+
+    import torch
+    import paper_1508_07828_b200 as pbn
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    pm = pbn.pbn_load(model)
+    chains, burn_in, window, batch = args.chains, args.burn_in, args.window, cfg.batch
+    chain_base = rank * chains                    # disjoint global chain ids per rank
+    out = pbn.alloc_outputs(pm, chains, window, batch=batch, emit_bits=True)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+
+    def one_step():
+        pbn.pbn_simulate(pm, out, n_chains=chains, chain_base=chain_base, steps=window,
+                         burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=True,
+                         emit_bits=True, groups_per_cta=args.groups, warps_per_group=args.warps,
+                         stream=stream)
+
+    for _ in range(args.warmup):
+        one_step()
+        flush.fill_(1)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    if rank == 0:
+        clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        one_step()
+        ev[k][1].record(stream)
+        flush.fill_(k)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    if dist:
+        t = torch.tensor([total_ms, max(kern_ms)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kmax = float(t[0]), float(t[1])
+    clk = clocks.stop() if rank == 0 else None
+
+    node_updates_per_step = chains * (burn_in + window) * model.n
+    value = world * node_updates_per_step * args.steps / (total_ms / 1e3)
+    chain_steps = world * chains * (burn_in + window) * args.steps / (total_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1 traj_kernel; one launch per step) ----
+    avg_kernel_s = statistics.mean(kern_ms) / 1e3
+    ops = algorithmic_alu_ops(model)
+    achieved = node_updates_per_step * ops / avg_kernel_s / 1e12       # T ALU-ops/s
+    sm_max = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            sm_max = float(json.load(f).get("sm_max_mhz", sm_max))
+    except Exception:
+        pass
+    peak = SM_COUNT_B200 * ALU_LANES_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_C4.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if tj.get("chains") == chains and tj.get("steps") == burn_in + window:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: same workload through the public API with HOST buffers ----
+    e2e = None
+    if rank == 0 or True:
+        rng = np.random.default_rng(cfg.sim_seed)
+        host_state = torch.from_numpy(
+            rng.integers(0, 2**32, size=(chains, pm.state_words), dtype=np.uint64)
+            .astype(np.uint32).view(np.int32)).pin_memory()
+        res_host = {k: torch.empty(tuple(getattr(out, k).shape), dtype=getattr(out, k).dtype).pin_memory()
+                    for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]}
+        h2d = host_state.numel() * 4
+        d2h = sum(t.numel() * t.element_size() for t in res_host.values())
+
+        def e2e_step():
+            out.state.copy_(host_state, non_blocking=True)
+            pbn.pbn_simulate(pm, out, n_chains=chains, chain_base=chain_base, steps=window,
+                             burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=False,
+                             emit_bits=True, stream=stream)
+            for k, t in res_host.items():
+                t.copy_(getattr(out, k), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t[0])
+        e2e = {"value": world * node_updates_per_step / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "pinned host state -> pbn_simulate -> all outputs to pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = ncores()
+        steps_s = 25_000 if model.n >= 1000 else 100_000
+        v, info = oracle_sample(model, pred, cfg.sim_seed, cores, steps_s, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{info['chains']} chains x {info['steps_per_chain']} transitions of "
+                         f"{cfg.key} ({info['seconds']:.1f} s wall, one thread per chain)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "chain_steps_per_s": chain_steps,
+            "config": workload_config(args, cfg, model),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "ops_per_node_update": ops,
+                         "peak_basis": f"{SM_COUNT_B200} SMs x {ALU_LANES_PER_CLK_PER_SM} ALU lanes/clk "
+                                       f"x {sm_max:.0f} MHz (guide unit counts; sm_max_mhz of "
+                                       f"MEASURED_PEAKS.json)",
+                         "kernel": "traj_kernel (K1)", "kernel_ms": statistics.mean(kern_ms)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

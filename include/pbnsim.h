@@ -1,0 +1,287 @@
+/*
+ * pbnsim.h -- C ABI of libpbnsim, the B200 (sm_100a) PBN trajectory engine.
+ *
+ * The hot path of Mizera, Pang & Yuan, "Parallel Approximate Steady-state
+ * Analysis of Large Probabilistic Boolean Networks" (arXiv 1508.07828):
+ * synchronous simulation of many independent PBN trajectories with fused
+ * per-chain statistics, plus the host statistics and driver that consume
+ * them.  Citations: P:n = line n of the paper's PAPER.md; readings Qn are
+ * listed in DESIGN.md.
+ *
+ * Conventions (all calls)
+ *   - No exceptions cross the ABI; every call returns a pbn_status.
+ *   - Host pointers are read during the call only; the caller keeps
+ *     ownership.  Device pointers are caller-allocated device memory (e.g.
+ *     torch tensors' data_ptr()) and are written asynchronously on the
+ *     caller's stream.
+ *   - A pbn_model owns only its device image; it is immutable after
+ *     pbn_load and may be used from several streams concurrently.
+ *   - Error text (when err != NULL) is NUL-terminated and truncated to errlen.
+ */
+#ifndef PBNSIM_H
+#define PBNSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PBN_OK = 0,
+    PBN_E_INVALID = 1,       /* model or predicate violates an invariant */
+    PBN_E_USAGE = 2,         /* bad arguments / unsupported size for this build   */
+    PBN_E_DEGENERATE = 3,    /* statistic undefined: W=0, alpha+beta in {0,2}, ... */
+    PBN_E_NOT_CONVERGED = 4, /* driver hit its step cap                            */
+    PBN_E_IO = 5,
+    PBN_E_CUDA = 6,          /* a CUDA runtime call failed                         */
+    PBN_E_NOMEM = 7
+} pbn_status;
+
+/* Perturbation semantics (reading Q1), chosen at load time. */
+enum {
+    PBN_PERTURB_VECTOR = 0,   /* any gamma_i(t)=1  =>  s(t+1) = s(t) XOR gamma(t) */
+    PBN_PERTURB_PER_NODE = 1  /* node i flips iff gamma_i(t)=1, else applies f     */
+};
+
+/* -------------------------------------------------------------------- */
+/* Model                                                     */
+/* -------------------------------------------------------------------- */
+typedef struct pbn_model_s* pbn_model;
+
+/* CSR description of a PBN G(V, F).  All arrays host memory.
+ *   n         1 <= n <= PBN_MAX_NODES
+ *   fn_off    [n+1]  node i owns functions fn_off[i] .. fn_off[i+1]-1;
+ *                    ell(i) = fn_off[i+1] - fn_off[i] >= 1
+ *   par_off   [nf+1] function f reads parents[par_off[f] .. par_off[f+1]-1]
+ *   parents   node ids < n, pairwise distinct per function; the FIRST
+ *             parent is the most significant bit of the table index (Q5)
+ *   tbl_off   [nf+1] in uint32 words; function f has ceil(2^theta/32) words
+ *   tables    entry idx of function f is bit (idx & 31) of word
+ *             tables[tbl_off[f] + (idx >> 5)]; bit 0 of word 0 = all parents 0
+ *   sel_prob  [nf]   c_j^(i) in (0,1]; per node the sum is within 1e-9 of 1
+ *   p         perturbation probability, 2^-32 <= p < 1
+ *   flags     PBN_PERTURB_* */
+typedef struct {
+    int32_t n;
+    const int32_t* fn_off;
+    const int32_t* par_off;
+    const uint16_t* parents;
+    const int32_t* tbl_off;
+    const uint32_t* tables;
+    const double* sel_prob;
+    double p;
+    uint32_t flags;
+} pbn_model_desc;
+
+#define PBN_MAX_NODES 16383   /* parent addresses are 16-bit byte offsets      */
+#define PBN_MAX_THETA 16      /* parents per predictor function                */
+#define PBN_MAX_ELL   128     /* predictor functions per node                  */
+#define PBN_MAX_PRED  16      /* (node, value) pairs in a property             */
+
+/* Host-only validation: returns PBN_OK or PBN_E_INVALID with a
+ * message naming the node and the violated rule.  Needs no GPU. */
+pbn_status pbn_validate(const pbn_model_desc* desc, char* err, size_t errlen);
+
+/* Validate, quantise p and c to 2^-32 (reading Q3), build the device image
+ * and upload it to `device` (the current device if device < 0).
+ * *out receives an opaque handle; release it with pbn_free. */
+pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char* err,
+                    size_t errlen);
+void pbn_free(pbn_model model);
+
+typedef struct {
+    int32_t n;
+    int32_t nf;             /* total predictor functions                        */
+    int64_t n_parents;      /* sum of theta over all functions                  */
+    double density;         /* D(G) = (1/n) sum_f theta(f)        */
+    uint32_t T_p;           /* floor(p 2^32)                                    */
+    uint32_t flags;
+    int32_t max_ell;
+    int32_t max_theta;
+    int64_t image_bytes;    /* device image size                                */
+} pbn_model_info;
+
+pbn_status pbn_get_model_info(pbn_model model, pbn_model_info* info);
+
+/* -------------------------------------------------------------------- */
+/* Trajectories with fused statistics              */
+/* -------------------------------------------------------------------- */
+
+/* Property = conjunction of k <= 16 (node, value) pairs.
+ * k = 0 means every state is in meta state 1.  Host pointers. */
+typedef struct {
+    int32_t k;
+    const uint16_t* node;
+    const uint8_t* value;
+} pbn_predicate;
+
+/* One call continues chains chain_base .. chain_base+n_chains-1 (global ids,
+ * < 2^32) from s_{step0} and performs burn_in + steps synchronous
+ * transitions.  Transition t (s_{t-1} -> s_t) uses the words
+ *     u(chain, t, i) = Philox4x32-10(counter = (i/4, chain, t mod 2^32, t >> 32),
+ *                                    key = (seed mod 2^32, seed >> 32))[i mod 4]
+ * (reading Q2), so outputs are independent of launch shape and of how
+ * chains and steps are split into calls (A12).  The recorded window is
+ * s_{step0+burn_in+1} .. s_{step0+burn_in+steps} (reading Q6).
+ *   init         1: ignore the input state and set s_0[i] = u(chain,0,i) >> 31
+ *                (requires step0 == 0; reading Q4)
+ *   batch        kappa >= 1 for batch sums of consecutive kappa-blocks of the
+ *                window (Fig. 2); 0 = none
+ *   emit_bits    1: write the window's indicator bits
+ *   bits_offset  window element w goes to bit (bits_offset + w) of its row,
+ *                so successive calls can append to one bitstream; the word
+ *                holding bit bits_offset is OR-merged (its bits below
+ *                bits_offset are kept, bits above must be 0), every other
+ *                touched word is overwritten
+ *   bits_row_words  row stride of `bits` in u32 (0 = ceil(steps/32))
+ *   groups_per_cta, warps_per_group: launch-shape overrides (0 = auto);
+ *                results never depend on them. */
+typedef struct {
+    int64_t n_chains;
+    int64_t chain_base;
+    int64_t step0;
+    int64_t burn_in;
+    int64_t steps;
+    int64_t batch;
+    uint64_t seed;
+    pbn_predicate pred;
+    int32_t init;
+    int32_t emit_bits;
+    int64_t bits_offset;
+    int64_t bits_row_words;
+    int32_t groups_per_cta;
+    int32_t warps_per_group;
+} pbn_sim_args;
+
+/* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).
+ *   state       [n_chains x ceil(n/32)] u32, in/out; node i of chain c is
+ *               bit (i & 31) of word state[c*ceil(n/32) + (i >> 5)]
+ *   c1          [n_chains] number of window states in meta state 1
+ *   n01, n10    [n_chains] 0->1 / 1->0 transitions between consecutive
+ *               window elements (pairs inside the window only, Q7)
+ *   first_last  [n_chains] bit 0 = I of the first window element, bit 1 = last
+ *   batch_sums  [n_chains x ceil(steps/batch)] or NULL (last batch may be short)
+ *   bits        [n_chains x bits_row_words] or NULL; element w of the window
+ *               is bit (b & 31) of word b >> 5 of its row, b = bits_offset + w
+ *   totals      [6] u64, overwritten: S1 = sum c1, S2 = sum c1^2, sum n01,
+ *               sum n10, sum n0from, sum n1from, where n0from / n1from count
+ *               window elements with a successor that are 0 / 1 (A10).
+ * Any pointer except state may be NULL if not wanted (totals NULL skips A10). */
+typedef struct {
+    uint32_t* state;
+    uint32_t* c1;
+    uint32_t* n01;
+    uint32_t* n10;
+    uint8_t* first_last;
+    uint32_t* batch_sums;
+    uint32_t* bits;
+    uint64_t* totals;
+} pbn_sim_out;
+
+/* Enqueue the trajectory kernel on `cuda_stream` (a cudaStream_t; NULL =
+ * legacy default stream).  Asynchronous: the caller synchronises.  Errors:
+ * PBN_E_USAGE (bad sizes, init with step0 != 0, > 2^32 chains, model too
+ * large for shared memory), PBN_E_CUDA (launch failure). */
+pbn_status pbn_simulate(pbn_model model, const pbn_sim_args* args, const pbn_sim_out* out,
+                        void* cuda_stream);
+
+/* Recount (K2) window statistics of a sub-window [start, start+length) of a
+ * stored indicator bitstream (device) without re-simulation: used by the
+ * Algorithm 4 burn-in re-check and by Skart re-batching
+ * (P:368).  bits has row stride `row_words` u32 per chain.  Outputs
+ * as in pbn_sim_out (device, any may be NULL). */
+pbn_status pbn_recount(const uint32_t* bits, int64_t n_chains, int64_t row_words, int64_t start,
+                       int64_t length, int64_t batch, uint32_t* c1, uint32_t* n01, uint32_t* n10,
+                       uint8_t* first_last, uint32_t* batch_sums, uint64_t* totals,
+                       void* cuda_stream);
+
+/* -------------------------------------------------------------------- */
+/* Host statistics, fp64                              */
+/* -------------------------------------------------------------------- */
+
+/* Gelman & Rubin potential scale reduction factor (Alg 3) of
+ * omega >= 2 windows of length psi >= 2 over the 0/1 indicator, from
+ * S1 = sum_i c_i and S2 = sum_i c_i^2 (exact integers):
+ *   B = psi/(omega-1) sum (mu_i - mu)^2,  W = (1/omega) sum s_i^2 (divisor psi-1),
+ *   sigma2 = (1 - 1/psi) W + B/psi,       rhat = sqrt(sigma2 / W).
+ * PBN_E_DEGENERATE when W = 0 (all windows constant); outputs may be NULL. */
+pbn_status pbn_gelman_rubin(uint64_t S1, uint64_t S2, int64_t omega, int64_t psi, double* rhat,
+                            double* B, double* W, double* sigma2);
+
+/* Two-state Markov chain rule (Alg 1 line 8) from pooled counts:
+ * alpha = n01/n0from, beta = n10/n1from, then
+ *   M = ceil( log(eps (alpha+beta)/max(alpha,beta)) / log|1-alpha-beta| )
+ *   N = ceil( alpha beta (2-alpha-beta)/(alpha+beta)^3 * Phi^-1((1+s)/2)^2 / r^2 ).
+ * alpha+beta = 1 gives M = 1 (reading Q10).  PBN_E_DEGENERATE when n0from
+ * or n1from is 0 or alpha+beta is 0 or 2.  M_raw / N_raw are the values
+ * before ceil. */
+typedef struct {
+    double alpha, beta, M_raw, N_raw;
+    int64_t M, N;
+} pbn_two_state_result;
+
+pbn_status pbn_two_state(uint64_t n01, uint64_t n0from, uint64_t n10, uint64_t n1from, double r,
+                         double s, double eps, pbn_two_state_result* res);
+
+/* Standard normal quantile Phi^-1(q), 0 < q < 1 (|error| < 1e-15 relative). */
+double pbn_inv_norm_cdf(double q);
+/* Student-t quantile with df >= 1 degrees of freedom. */
+double pbn_t_quantile(double q, double df);
+
+/* Skart CI step (Alg 2 lines 10-14 / Alg 5 lines 13-16, P:372-382,
+ * P:564-575) over batch means of omega chains laid out chain-major
+ * (batches never straddle chains, Fig. 2b): given per-chain batch sums
+ * [omega x per_chain] of batch size kappa, returns the grand mean mu, the
+ * skewness- and autoregression-adjusted CI and H = max(mu-lo, hi-mu).
+ * Declared Skart constants per SPEC S:375 (reading Q11/Q12). */
+typedef struct {
+    double mu, var, phi, skew, ci_lo, ci_hi, H;
+    int64_t batches;
+} pbn_skart_ci;
+
+pbn_status pbn_skart_ci_from_batches(const uint32_t* batch_sums, int64_t omega, int64_t per_chain,
+                                     int64_t kappa, double alpha_conf, pbn_skart_ci* res);
+
+/* -------------------------------------------------------------------- */
+/* Host driver: Algorithm 3 then Algorithm 4 or 5           */
+/* -------------------------------------------------------------------- */
+enum { PBN_METHOD_TWO_STATE = 0, PBN_METHOD_SKART = 1 };
+
+typedef struct {
+    int32_t method;          /* PBN_METHOD_*                                     */
+    int64_t omega;           /* chains >= 2                                      */
+    int64_t psi0;            /* initial Gelman-Rubin half length (Alg 3)         */
+    double rhat_threshold;   /* "close to 1": stop when rhat < threshold (Q8)    */
+    double r, s, eps;        /* two-state precision, confidence, epsilon         */
+    double h_star, alpha_conf; /* Skart precision and confidence parameter       */
+    uint64_t seed;
+    pbn_predicate pred;
+    int64_t max_steps;       /* per-chain step cap (PBN_E_NOT_CONVERGED)         */
+} pbn_run_args;
+
+typedef struct {
+    double estimate;         /* steady-state probability of the property         */
+    double ci_lo, ci_hi;     /* Skart only                                       */
+    double rhat;             /* last R-hat (the one that passed)                 */
+    int64_t psi;             /* burn-in psi returned by Alg 3 (after Alg 4 re-check) */
+    int64_t sample_size;     /* pooled elements used by the estimate             */
+    int64_t steps_per_chain; /* total transitions simulated per chain            */
+    int64_t gr_iterations;
+    int64_t extensions;
+    int64_t M, N;            /* last two-state burn-in / sample size             */
+    double alpha, beta;
+} pbn_run_result;
+
+pbn_status pbn_run(pbn_model model, const pbn_run_args* args, pbn_run_result* res,
+                   void* cuda_stream, char* err, size_t errlen);
+
+/* Version string of the build, e.g. "libpbnsim 0.1 sm_100a". */
+const char* pbn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBNSIM_H */

@@ -1,0 +1,652 @@
+// pbn_api.cpp -- host side of libpbnsim: validation, device-image builder,
+// launch wrappers, fp64 statistics and the Algorithm 3/4/5 driver.
+//
+// C ABI declared in include/pbnsim.h.  Nothing here is shared with oracle/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pbnsim.h"
+#include "pbn_internal.h"
+
+struct pbn_model_s {
+    int device = 0;
+    pbn::ImageLayout L;
+    uint8_t* d_image = nullptr;
+    uint32_t Tp = 0;
+    uint32_t flags = 0;
+    int64_t n_parents = 0;
+};
+
+namespace {
+
+void set_err(char* err, size_t errlen, const char* fmt, ...)
+{
+    if (!err || errlen == 0) return;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, errlen, fmt, ap);
+    va_end(ap);
+}
+
+constexpr uint64_t kTwo32 = 1ull << 32;
+
+uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// ---------------------------------------------------------------------
+// Reading Q3: the 32-bit word scheme.  T_p = floor(p 2^32); for the j-th
+// cumulative selection probability C_j (left-to-right fp64 sum) of a node,
+// Q_j = min(floor(C_j 2^32), 2^32) and D_j = T_p + floor(Q_j (2^32 - T_p) / 2^32).
+// Function j (0-based) is chosen iff D_j <= u < D_{j+1}; the kernel uses
+// E_j = D_j - 1 and counts j = #{k : u > E_k}.
+// ---------------------------------------------------------------------
+uint32_t quantise_p(double p) { return (uint32_t)std::floor(std::ldexp(p, 32)); }
+
+uint32_t boundary_E(double cum, uint32_t Tp)
+{
+    double q = std::floor(std::ldexp(cum, 32));
+    uint64_t Q = q >= (double)kTwo32 ? kTwo32 : (uint64_t)q;
+    const unsigned __int128 prod = (unsigned __int128)Q * (unsigned __int128)(kTwo32 - Tp);
+    const uint64_t D = (uint64_t)Tp + (uint64_t)(prod >> 32);  // 1 <= D <= 2^32
+    return (uint32_t)(D - 1);
+}
+
+pbn_status validate(const pbn_model_desc* d, char* err, size_t errlen)
+{
+    if (!d) {
+        set_err(err, errlen, "null model description");
+        return PBN_E_INVALID;
+    }
+    if (d->n < 1) {
+        set_err(err, errlen, "n must be >= 1 (got %d)", d->n);
+        return PBN_E_INVALID;
+    }
+    if (!d->fn_off || !d->par_off || !d->tbl_off || !d->tables || !d->sel_prob) {
+        set_err(err, errlen, "null array in model description");
+        return PBN_E_INVALID;
+    }
+    if (!(d->p >= std::ldexp(1.0, -32) && d->p < 1.0)) {
+        set_err(err, errlen, "perturbation p must satisfy 2^-32 <= p < 1 (got %.17g)", d->p);
+        return PBN_E_INVALID;
+    }
+    if (d->flags > PBN_PERTURB_PER_NODE) {
+        set_err(err, errlen, "unknown flags %u", d->flags);
+        return PBN_E_INVALID;
+    }
+    if (d->fn_off[0] != 0) {
+        set_err(err, errlen, "fn_off[0] must be 0");
+        return PBN_E_INVALID;
+    }
+    for (int32_t i = 0; i < d->n; ++i) {
+        const int32_t f0 = d->fn_off[i], f1 = d->fn_off[i + 1];
+        if (f1 <= f0) {
+            set_err(err, errlen, "node %d: needs at least one predictor function (ell >= 1)", i);
+            return PBN_E_INVALID;
+        }
+        double sum = 0.0;
+        for (int32_t f = f0; f < f1; ++f) {
+            const double c = d->sel_prob[f];
+            if (!(c > 0.0 && c <= 1.0)) {
+                set_err(err, errlen, "node %d: selection probability of function %d must be in (0,1] (got %.17g)",
+                        i, f - f0, c);
+                return PBN_E_INVALID;
+            }
+            sum += c;
+            const int32_t p0 = d->par_off[f], p1 = d->par_off[f + 1];
+            if (p1 < p0) {
+                set_err(err, errlen, "node %d: function %d has negative parent count", i, f - f0);
+                return PBN_E_INVALID;
+            }
+            const int32_t theta = p1 - p0;
+            if (theta > 0 && !d->parents) {
+                set_err(err, errlen, "null parents array");
+                return PBN_E_INVALID;
+            }
+            for (int32_t a = p0; a < p1; ++a) {
+                if ((int32_t)d->parents[a] >= d->n) {
+                    set_err(err, errlen, "node %d: function %d parent %u out of range (n=%d)", i, f - f0,
+                            (unsigned)d->parents[a], d->n);
+                    return PBN_E_INVALID;
+                }
+                for (int32_t b = p0; b < a; ++b)
+                    if (d->parents[a] == d->parents[b]) {
+                        set_err(err, errlen, "node %d: function %d repeats parent %u", i, f - f0,
+                                (unsigned)d->parents[a]);
+                        return PBN_E_INVALID;
+                    }
+            }
+            if (theta > 30) {
+                set_err(err, errlen, "node %d: function %d has %d parents (> 30)", i, f - f0, theta);
+                return PBN_E_INVALID;
+            }
+            const int64_t words = ((int64_t)1 << theta) <= 32 ? 1 : ((int64_t)1 << theta) / 32;
+            if ((int64_t)d->tbl_off[f + 1] - d->tbl_off[f] != words) {
+                set_err(err, errlen, "node %d: function %d table has %d words, expected %lld for %d parents", i,
+                        f - f0, d->tbl_off[f + 1] - d->tbl_off[f], (long long)words, theta);
+                return PBN_E_INVALID;
+            }
+        }
+        if (std::fabs(sum - 1.0) > 1e-9) {
+            set_err(err, errlen, "node %d: selection probabilities sum to %.17g, not 1 (+-1e-9)", i, sum);
+            return PBN_E_INVALID;
+        }
+    }
+    return PBN_OK;
+}
+
+// Limits of the device kernels (beyond model validity).
+pbn_status check_device_limits(const pbn_model_desc* d, char* err, size_t errlen)
+{
+    if (d->n > PBN_MAX_NODES) {
+        set_err(err, errlen, "n=%d exceeds PBN_MAX_NODES=%d of this build", d->n, PBN_MAX_NODES);
+        return PBN_E_USAGE;
+    }
+    const int32_t nf = d->fn_off[d->n];
+    if (nf >= (1 << 20)) {
+        set_err(err, errlen, "%d predictor functions exceed 2^20-1", nf);
+        return PBN_E_USAGE;
+    }
+    for (int32_t i = 0; i < d->n; ++i) {
+        const int32_t ell = d->fn_off[i + 1] - d->fn_off[i];
+        if (ell > PBN_MAX_ELL) {
+            set_err(err, errlen, "node %d: %d functions exceed PBN_MAX_ELL=%d", i, ell, PBN_MAX_ELL);
+            return PBN_E_USAGE;
+        }
+        for (int32_t f = d->fn_off[i]; f < d->fn_off[i + 1]; ++f)
+            if (d->par_off[f + 1] - d->par_off[f] > PBN_MAX_THETA) {
+                set_err(err, errlen, "node %d: function with %d parents exceeds PBN_MAX_THETA=%d", i,
+                        d->par_off[f + 1] - d->par_off[f], PBN_MAX_THETA);
+                return PBN_E_USAGE;
+            }
+    }
+    return PBN_OK;
+}
+
+// Device image (layout: pbn_internal.h).
+std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L)
+{
+    const int32_t n = d->n, nf = d->fn_off[n];
+    int32_t max_ell = 0, max_theta = 0;
+    int64_t aux_words = 0;
+    for (int32_t i = 0; i < n; ++i) max_ell = std::max(max_ell, d->fn_off[i + 1] - d->fn_off[i]);
+    for (int32_t f = 0; f < nf; ++f) {
+        const int32_t theta = d->par_off[f + 1] - d->par_off[f];
+        max_theta = std::max(max_theta, theta);
+        aux_words += (theta + 1) / 2;
+        if (theta >= 6) aux_words += ((int64_t)1 << theta) / 32;
+    }
+    aux_words += 4;  // slack: reads never leave the section
+    L->n = n;
+    L->nf = nf;
+    L->aux_words = (int32_t)aux_words;
+    L->has_xthr = max_ell > 4;
+    L->max_theta = max_theta;
+    L->max_ell = max_ell;
+    L->off_nrec = 0;
+    L->off_fdesc = align16(L->off_nrec + 16u * n);
+    L->off_aux = align16(L->off_fdesc + 8u * nf);
+    L->off_xthr = align16(L->off_aux + 4u * (uint32_t)aux_words);
+    L->bytes = align16(L->off_xthr + (L->has_xthr ? 4u * nf : 0u));
+
+    std::vector<uint8_t> img(L->bytes, 0);
+    uint32_t* nrec = reinterpret_cast<uint32_t*>(img.data() + L->off_nrec);
+    uint32_t* fdesc = reinterpret_cast<uint32_t*>(img.data() + L->off_fdesc);
+    uint32_t* aux = reinterpret_cast<uint32_t*>(img.data() + L->off_aux);
+    uint32_t* xthr = reinterpret_cast<uint32_t*>(img.data() + L->off_xthr);
+    uint32_t ap = 0;  // aux cursor (u32)
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t f0 = d->fn_off[i], f1 = d->fn_off[i + 1];
+        const int32_t ell = f1 - f0;
+        uint32_t E[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+        double cum = 0.0;
+        int32_t thmax = 0;
+        for (int32_t j = 0; j < ell; ++j) {
+            const int32_t f = f0 + j;
+            cum += d->sel_prob[f];
+            if (j < ell - 1) {
+                const uint32_t e = boundary_E(cum, Tp);
+                if (j < 3) E[j] = e;
+                if (L->has_xthr) xthr[f] = e;  // xthr[fn_base + k - 1] = E_k
+            }
+            const int32_t theta = d->par_off[f + 1] - d->par_off[f];
+            thmax = std::max(thmax, theta);
+            // descriptor
+            uint32_t t0 = 0;
+            if (theta <= 5) t0 = d->tables[d->tbl_off[f]];
+            fdesc[2 * f + 0] = t0;
+            fdesc[2 * f + 1] = (uint32_t)theta | (ap << 5);
+            // parents reversed: half-word m = parents[theta-1-m] as byte offset
+            uint16_t* h = reinterpret_cast<uint16_t*>(aux + ap);
+            for (int32_t m = 0; m < theta; ++m)
+                h[m] = (uint16_t)(4u * d->parents[d->par_off[f] + theta - 1 - m]);
+            ap += (uint32_t)(theta + 1) / 2;
+            if (theta >= 6) {
+                const int32_t words = (1 << theta) / 32;
+                for (int32_t w = 0; w < words; ++w) aux[ap + w] = d->tables[d->tbl_off[f] + w];
+                ap += (uint32_t)words;
+            }
+        }
+        nrec[4 * i + 0] = E[0];
+        nrec[4 * i + 1] = E[1];
+        nrec[4 * i + 2] = E[2];
+        nrec[4 * i + 3] = (uint32_t)f0 | ((uint32_t)thmax << 20) | ((uint32_t)(ell - 1) << 25);
+    }
+    return img;
+}
+
+pbn_status cuda_status(cudaError_t e, char* err, size_t errlen, const char* what)
+{
+    if (e == cudaSuccess) return PBN_OK;
+    set_err(err, errlen, "%s: %s", what, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? PBN_E_NOMEM : PBN_E_CUDA;
+}
+
+// Declared Skart constants (reading Q11).
+constexpr double kSkartClamp = 0.999999;
+
+}  // namespace
+
+// =====================================================================
+// C ABI
+// =====================================================================
+extern "C" {
+
+const char* pbn_version(void) { return "libpbnsim 0.1 sm_100a"; }
+
+pbn_status pbn_validate(const pbn_model_desc* desc, char* err, size_t errlen)
+{
+    return validate(desc, err, errlen);
+}
+
+pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char* err, size_t errlen)
+{
+    if (!out) {
+        set_err(err, errlen, "null output handle");
+        return PBN_E_USAGE;
+    }
+    *out = nullptr;
+    pbn_status st = validate(desc, err, errlen);
+    if (st != PBN_OK) return st;
+    st = check_device_limits(desc, err, errlen);
+    if (st != PBN_OK) return st;
+    if (device < 0) {
+        cudaError_t e = cudaGetDevice(&device);
+        if (e != cudaSuccess) return cuda_status(e, err, errlen, "cudaGetDevice");
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_status(e, err, errlen, "cudaSetDevice");
+    auto* m = new pbn_model_s();
+    m->device = device;
+    m->flags = desc->flags;
+    m->Tp = quantise_p(desc->p);
+    m->n_parents = desc->par_off[desc->fn_off[desc->n]];
+    std::vector<uint8_t> img = build_image(desc, m->Tp, &m->L);
+    e = cudaMalloc(&m->d_image, img.size());
+    if (e != cudaSuccess) {
+        delete m;
+        return cuda_status(e, err, errlen, "cudaMalloc(image)");
+    }
+    e = cudaMemcpy(m->d_image, img.data(), img.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(m->d_image);
+        delete m;
+        return cuda_status(e, err, errlen, "cudaMemcpy(image)");
+    }
+    *out = m;
+    return PBN_OK;
+}
+
+void pbn_free(pbn_model model)
+{
+    if (!model) return;
+    if (model->d_image) cudaFree(model->d_image);
+    delete model;
+}
+
+pbn_status pbn_get_model_info(pbn_model m, pbn_model_info* info)
+{
+    if (!m || !info) return PBN_E_USAGE;
+    info->n = m->L.n;
+    info->nf = m->L.nf;
+    info->n_parents = m->n_parents;
+    info->density = (double)m->n_parents / (double)m->L.n;
+    info->T_p = m->Tp;
+    info->flags = m->flags;
+    info->max_ell = m->L.max_ell;
+    info->max_theta = m->L.max_theta;
+    info->image_bytes = m->L.bytes;
+    return PBN_OK;
+}
+
+static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o,
+                                   pbn::TrajParams* P)
+{
+    if (!m || !a || !o || !o->state) return PBN_E_USAGE;
+    if (a->n_chains < 0 || a->chain_base < 0 || a->step0 < 0 || a->burn_in < 0 || a->steps < 0 ||
+        a->batch < 0)
+        return PBN_E_USAGE;
+    if (a->chain_base + a->n_chains > (int64_t)kTwo32) return PBN_E_USAGE;
+    if (a->steps >= (int64_t)kTwo32) return PBN_E_USAGE;  // u32 counters
+    if (a->init && a->step0 != 0) return PBN_E_USAGE;
+    if (a->pred.k < 0 || a->pred.k > PBN_MAX_PRED) return PBN_E_USAGE;
+    if (a->pred.k > 0 && (!a->pred.node || !a->pred.value)) return PBN_E_USAGE;
+    if (a->steps > 0 && a->batch > 0 && !o->batch_sums) return PBN_E_USAGE;
+    if (a->steps > 0 && a->emit_bits && !o->bits) return PBN_E_USAGE;
+    if (a->bits_offset < 0 || a->bits_row_words < 0) return PBN_E_USAGE;
+    std::memset(P, 0, sizeof(*P));
+    P->image = m->d_image;
+    P->L = m->L;
+    P->Tp = m->Tp;
+    P->per_node = m->flags == PBN_PERTURB_PER_NODE;
+    P->n = m->L.n;
+    P->nquads = (m->L.n + 3) / 4;
+    P->n_pad = (m->L.n + 3) & ~3;
+    P->state_words = (m->L.n + 31) / 32;
+    P->group_stride = (P->per_node ? 2 : 3) * P->n_pad + 32;
+    P->seed = a->seed;
+    P->n_chains = a->n_chains;
+    P->chain_base = a->chain_base;
+    P->step0 = a->step0;
+    P->burn_in = a->burn_in;
+    P->steps = a->steps;
+    P->batch = a->batch;
+    P->init = a->init ? 1 : 0;
+    P->emit_bits = a->emit_bits ? 1 : 0;
+    P->pred_k = a->pred.k;
+    for (int k = 0; k < a->pred.k; ++k) {
+        if ((int32_t)a->pred.node[k] >= m->L.n || a->pred.value[k] > 1) return PBN_E_INVALID;
+        P->pred_node[k] = a->pred.node[k];
+        P->pred_val[k] = a->pred.value[k];
+    }
+    P->batch_row = a->batch > 0 ? (a->steps + a->batch - 1) / a->batch : 0;
+    const int64_t need_words = (a->bits_offset + a->steps + 31) / 32;
+    P->bits_row = a->bits_row_words > 0 ? a->bits_row_words : (a->steps + 31) / 32;
+    if (a->emit_bits && a->steps > 0 && P->bits_row < need_words) return PBN_E_USAGE;
+    P->bits_offset = a->bits_offset;
+    P->state = o->state;
+    P->c1 = o->c1;
+    P->n01 = o->n01;
+    P->n10 = o->n10;
+    P->first_last = o->first_last;
+    P->batch_sums = o->batch_sums;
+    P->bits = o->bits;
+    P->totals = reinterpret_cast<unsigned long long*>(o->totals);
+    return PBN_OK;
+}
+
+pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o, void* stream)
+{
+    pbn::TrajParams P;
+    pbn_status st = fill_traj_params(m, a, o, &P);
+    if (st != PBN_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (o->totals) {
+        if (cudaMemsetAsync(o->totals, 0, 6 * sizeof(uint64_t), s) != cudaSuccess) return PBN_E_CUDA;
+    }
+    if (a->n_chains == 0) return PBN_OK;
+    pbn::LaunchPlan plan;
+    const char* why = nullptr;
+    int rc = pbn::plan_traj_launch(P, m->device, a->groups_per_cta, a->warps_per_group, &plan, &why);
+    if (rc < 0) return PBN_E_USAGE;
+    if (rc > 0) return PBN_E_CUDA;
+    rc = pbn::launch_traj(P, plan, stream);
+    return rc == 0 ? PBN_OK : PBN_E_CUDA;
+}
+
+pbn_status pbn_recount(const uint32_t* bits, int64_t n_chains, int64_t row_words, int64_t start,
+                       int64_t length, int64_t batch, uint32_t* c1, uint32_t* n01, uint32_t* n10,
+                       uint8_t* first_last, uint32_t* batch_sums, uint64_t* totals, void* stream)
+{
+    if (!bits || n_chains < 0 || row_words <= 0 || start < 0 || length < 0 || batch < 0)
+        return PBN_E_USAGE;
+    if ((start + length + 31) / 32 > row_words) return PBN_E_USAGE;
+    if (batch > 0 && !batch_sums) return PBN_E_USAGE;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (totals && cudaMemsetAsync(totals, 0, 6 * sizeof(uint64_t), s) != cudaSuccess) return PBN_E_CUDA;
+    pbn::RecountParams R;
+    R.bits = bits;
+    R.n_chains = n_chains;
+    R.row_words = row_words;
+    R.start = start;
+    R.length = length;
+    R.batch = batch;
+    R.batch_row = batch > 0 ? (length + batch - 1) / batch : 0;
+    R.c1 = c1;
+    R.n01 = n01;
+    R.n10 = n10;
+    R.first_last = first_last;
+    R.batch_sums = batch_sums;
+    R.totals = reinterpret_cast<unsigned long long*>(totals);
+    return pbn::launch_recount(R, stream) == 0 ? PBN_OK : PBN_E_CUDA;
+}
+
+// ---------------------------------------------------------------------
+// Gelman & Rubin (Alg 3) from exact integer sums:
+//   B = (omega S2 - S1^2) / (omega psi (omega-1))
+//   W = (psi S1 - S2) / (omega psi (psi-1))
+// both numerators formed exactly in 128-bit integers.
+// ---------------------------------------------------------------------
+pbn_status pbn_gelman_rubin(uint64_t S1, uint64_t S2, int64_t omega, int64_t psi, double* rhat,
+                            double* B, double* W, double* sigma2)
+{
+    if (omega < 2 || psi < 2) return PBN_E_USAGE;
+    const unsigned __int128 om = (unsigned __int128)omega, ps = (unsigned __int128)psi;
+    const unsigned __int128 s1 = S1, s2 = S2;
+    const unsigned __int128 bn_a = om * s2, bn_b = s1 * s1;
+    const unsigned __int128 wn_a = ps * s1;
+    if (bn_a < bn_b || wn_a < s2) return PBN_E_USAGE;  // inconsistent sums
+    const double Bv = (double)(bn_a - bn_b) / ((double)omega * (double)psi * (double)(omega - 1));
+    const double Wv = (double)(wn_a - s2) / ((double)omega * (double)psi * (double)(psi - 1));
+    const double s2v = (1.0 - 1.0 / (double)psi) * Wv + Bv / (double)psi;
+    if (B) *B = Bv;
+    if (W) *W = Wv;
+    if (sigma2) *sigma2 = s2v;
+    if (Wv == 0.0) {
+        if (rhat) *rhat = NAN;
+        return PBN_E_DEGENERATE;
+    }
+    if (rhat) *rhat = std::sqrt(s2v / Wv);
+    return PBN_OK;
+}
+
+// ---------------------------------------------------------------------
+// Phi^-1: Abramowitz & Stegun 26.2.23 start, then Halley steps on erfc.
+// ---------------------------------------------------------------------
+double pbn_inv_norm_cdf(double q)
+{
+    if (!(q > 0.0 && q < 1.0)) return NAN;
+    if (q > 0.5) return -pbn_inv_norm_cdf(1.0 - q);
+    const double t = std::sqrt(-2.0 * std::log(q));
+    double x = -(t - (2.515517 + 0.802853 * t + 0.010328 * t * t) /
+                         (1.0 + 1.432788 * t + 0.189269 * t * t + 0.001308 * t * t * t));
+    const double rt2pi = 2.5066282746310002;  // sqrt(2 pi)
+    for (int it = 0; it < 4; ++it) {
+        const double e = 0.5 * std::erfc(-x / 1.4142135623730951) - q;
+        const double u = e * rt2pi * std::exp(0.5 * x * x);
+        x = x - u / (1.0 + 0.5 * x * u);
+    }
+    return x;
+}
+
+// Regularised incomplete beta I_x(a,b) by the modified Lentz continued fraction.
+static double betacf(double a, double b, double x)
+{
+    const double tiny = 1e-300, eps = 1e-16;
+    double qab = a + b, qap = a + 1.0, qam = a - 1.0;
+    double c = 1.0, d = 1.0 - qab * x / qap;
+    if (std::fabs(d) < tiny) d = tiny;
+    d = 1.0 / d;
+    double h = d;
+    for (int m = 1; m <= 10000; ++m) {
+        const int m2 = 2 * m;
+        double aa = m * (b - m) * x / ((qam + m2) * (a + m2));
+        d = 1.0 + aa * d;
+        if (std::fabs(d) < tiny) d = tiny;
+        c = 1.0 + aa / c;
+        if (std::fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        h *= d * c;
+        aa = -(a + m) * (qab + m) * x / ((a + m2) * (qap + m2));
+        d = 1.0 + aa * d;
+        if (std::fabs(d) < tiny) d = tiny;
+        c = 1.0 + aa / c;
+        if (std::fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (std::fabs(del - 1.0) < eps) break;
+    }
+    return h;
+}
+
+// Stirling remainder lgamma(z) - [(z-1/2) ln z - z + ln(2 pi)/2], z >= 10.
+static double stirling_delta(double z)
+{
+    const double r = 1.0 / z, r2 = r * r;
+    return r * (1.0 / 12.0 - r2 * (1.0 / 360.0 - r2 * (1.0 / 1260.0 - r2 * (1.0 / 1680.0))));
+}
+
+// lgamma(a+b) - lgamma(a) - lgamma(b) without cancellation when a is large.
+static double log_inv_beta(double a, double b)
+{
+    if (a < 10.0) return std::lgamma(a + b) - std::lgamma(a) - std::lgamma(b);
+    return (a - 0.5) * std::log1p(b / a) + b * std::log(a + b) - b + stirling_delta(a + b) -
+           stirling_delta(a) - std::lgamma(b);
+}
+
+// I_x(a,b) given both x and y = 1 - x (each computed without cancellation).
+static double inc_beta(double a, double b, double x, double y)
+{
+    if (x <= 0.0) return 0.0;
+    if (y <= 0.0) return 1.0;
+    const double big = std::max(a, b), small = std::min(a, b);
+    const double lbt = log_inv_beta(big, small) + a * std::log(x) + b * std::log(y);
+    const double bt = std::exp(lbt);
+    if (x < (a + 1.0) / (a + b + 2.0)) return bt * betacf(a, b, x) / a;
+    return 1.0 - bt * betacf(b, a, y) / b;
+}
+
+// Student-t lower tail probability P(T <= t) for t <= 0:
+// 0.5 I_{df/(df+t^2)}(df/2, 1/2).
+static double t_lower_tail(double t, double df)
+{
+    const double den = df + t * t;
+    return 0.5 * inc_beta(0.5 * df, 0.5, df / den, (t * t) / den);
+}
+
+double pbn_t_quantile(double q, double df)
+{
+    if (!(q > 0.0 && q < 1.0) || !(df >= 1.0)) return NAN;
+    if (q > 0.5) return -pbn_t_quantile(1.0 - q, df);
+    if (q == 0.5) return 0.0;
+    if (df == 1.0) return std::tan(M_PI * (q - 0.5));
+    // Newton on the lower tail from the normal quantile, safeguarded by bisection
+    double x = pbn_inv_norm_cdf(q);
+    double lo = -1e300, hi = 0.0;
+    const double lgc = std::lgamma(0.5 * (df + 1.0)) - std::lgamma(0.5 * df) - 0.5 * std::log(df * M_PI);
+    for (int it = 0; it < 200; ++it) {
+        const double F = t_lower_tail(x, df);
+        const double f = F - q;
+        if (f > 0.0) hi = std::min(hi, x);
+        else lo = std::max(lo, x);
+        const double pdf = std::exp(lgc - 0.5 * (df + 1.0) * std::log1p(x * x / df));
+        double nx = x - f / pdf;
+        if (!(nx > lo && nx < hi)) nx = (lo > -1e299) ? 0.5 * (lo + hi) : 2.0 * x - 1.0;
+        if (std::fabs(nx - x) <= 1e-15 * std::max(1.0, std::fabs(x))) {
+            x = nx;
+            break;
+        }
+        x = nx;
+    }
+    return x;
+}
+
+pbn_status pbn_two_state(uint64_t n01, uint64_t n0from, uint64_t n10, uint64_t n1from, double r,
+                         double s, double eps, pbn_two_state_result* res)
+{
+    if (!res || !(r > 0.0) || !(s > 0.0 && s < 1.0) || !(eps > 0.0)) return PBN_E_USAGE;
+    res->alpha = res->beta = res->M_raw = res->N_raw = NAN;
+    res->M = res->N = 0;
+    if (n0from == 0 || n1from == 0) return PBN_E_DEGENERATE;
+    const double a = (double)n01 / (double)n0from;
+    const double b = (double)n10 / (double)n1from;
+    res->alpha = a;
+    res->beta = b;
+    const double apb = a + b;
+    if (apb == 0.0 || apb == 2.0) return PBN_E_DEGENERATE;
+    const double lam = std::fabs(1.0 - apb);
+    const double M_raw = lam == 0.0 ? 1.0 : std::log(eps * apb / std::max(a, b)) / std::log(lam);
+    const double z = pbn_inv_norm_cdf(0.5 * (1.0 + s));
+    const double N_raw = (a * b * (2.0 - apb) / (apb * apb * apb)) * (z * z / (r * r));
+    res->M_raw = M_raw;
+    res->N_raw = N_raw;
+    res->M = (int64_t)std::ceil(M_raw);
+    res->N = (int64_t)std::ceil(N_raw);
+    return PBN_OK;
+}
+
+// ---------------------------------------------------------------------
+// Skart CI (readings Q11/Q12) over chain-major batch means.
+// ---------------------------------------------------------------------
+pbn_status pbn_skart_ci_from_batches(const uint32_t* bs, int64_t omega, int64_t per_chain, int64_t kappa,
+                                     double alpha_conf, pbn_skart_ci* res)
+{
+    if (!bs || !res || omega < 1 || per_chain < 1 || kappa < 1 || !(alpha_conf > 0.0 && alpha_conf < 1.0))
+        return PBN_E_USAGE;
+    const int64_t P = omega * per_chain;
+    if (P < 3) return PBN_E_USAGE;
+    // batch means and their moments (mean, variance with divisor P-1)
+    long double sum = 0.0L;
+    for (int64_t j = 0; j < P; ++j) sum += (long double)bs[j];
+    const double mu = (double)(sum / (long double)P) / (double)kappa;
+    double m2 = 0.0, m3 = 0.0, lag = 0.0;
+    for (int64_t j = 0; j < P; ++j) {
+        const double y = (double)bs[j] / (double)kappa - mu;
+        m2 += y * y;
+        m3 += y * y * y;
+    }
+    for (int64_t c = 0; c < omega; ++c)
+        for (int64_t k = 0; k + 1 < per_chain; ++k) {  // no cross-chain pairs (Q12)
+            const int64_t j = c * per_chain + k;
+            lag += ((double)bs[j] / (double)kappa - mu) * ((double)bs[j + 1] / (double)kappa - mu);
+        }
+    res->batches = P;
+    res->mu = mu;
+    if (m2 == 0.0) {
+        res->var = 0.0;
+        res->phi = 0.0;
+        res->skew = NAN;
+        res->ci_lo = res->ci_hi = mu;
+        res->H = 0.0;
+        return PBN_E_DEGENERATE;
+    }
+    const double var = m2 / (double)(P - 1);
+    double phi = lag / m2;
+    phi = std::max(-kSkartClamp, std::min(kSkartClamp, phi));
+    const double skew = (m3 / (double)P) / std::pow(m2 / (double)P, 1.5);
+    const double A = (1.0 + phi) / (1.0 - phi);
+    const double bhat = skew / (6.0 * std::sqrt((double)P));
+    auto G = [bhat](double t) {
+        if (bhat == 0.0) return t;
+        return (std::cbrt(1.0 + 6.0 * bhat * (t - bhat)) - 1.0) / (2.0 * bhat);
+    };
+    const double df = (double)(P - 1);
+    const double tl = pbn_t_quantile(0.5 * alpha_conf, df);
+    const double tu = pbn_t_quantile(1.0 - 0.5 * alpha_conf, df);
+    const double sc = std::sqrt(A * var / (double)P);
+    res->var = var;
+    res->phi = phi;
+    res->skew = skew;
+    res->ci_lo = mu + G(tl) * sc;
+    res->ci_hi = mu + G(tu) * sc;
+    res->H = std::max(mu - res->ci_lo, res->ci_hi - mu);
+    return PBN_OK;
+}
+
+}  // extern "C"

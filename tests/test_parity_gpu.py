@@ -1,0 +1,189 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact
+on every output field (state, c1, n01, n10, first/last, batch sums, bits,
+totals) -- BASELINE north_star: "GPU trajectories, counts and transition
+tallies must be bit-exact against the oracle".
+
+Small configs are compared on all chains; C3-C5 run in the exact launch
+configuration bench.py times and are compared on a deterministic sample of
+chains that the oracle computes one by one at the full step count.
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import compare_chain, gpu_run, oracle_run, pack_states, sample_chain_ids
+from oracle import stats as ostats
+from workloads import (CONFIGS, Predicate, config_model, config_predicate, model_from_lists,
+                       random_pbn)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pbn():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1508_07828_b200 as pbn
+    return pbn
+
+
+def load(pbn, model, per_node=False):
+    return pbn.pbn_load(model, per_node=per_node)
+
+
+def full_compare(pbn, model, pred, *, n_chains, steps, burn_in=0, seed=1, batch=0, per_node=False,
+                 groups=0, warps=0, threads=8):
+    pm = load(pbn, model, per_node)
+    g = gpu_run(pm, model, pred, n_chains=n_chains, steps=steps, burn_in=burn_in, seed=seed,
+                batch=batch, groups=groups, warps=warps)
+    st, I, ws = oracle_run(model, pred, np.arange(n_chains), steps=steps, burn_in=burn_in, seed=seed,
+                           batch=batch, per_node=per_node, threads=threads)
+    packed = pack_states(st)
+    for c in range(n_chains):
+        compare_chain(g, c, packed[c], ws[c], steps, batch)
+    assert np.array_equal(g["totals"], ostats.totals(ws))
+    return g
+
+
+def test_C1_all_fields_bit_exact(pbn):
+    c = CONFIGS["C1"]
+    full_compare(pbn, config_model("C1"), config_predicate("C1"), n_chains=c.chains, steps=c.steps,
+                 burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch)
+
+
+def test_C1_per_node_semantics(pbn):
+    c = CONFIGS["C1"]
+    full_compare(pbn, config_model("C1"), config_predicate("C1"), n_chains=c.chains, steps=c.steps,
+                 burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch, per_node=True)
+
+
+def test_C2_all_chains(pbn):
+    c = CONFIGS["C2"]
+    full_compare(pbn, config_model("C2"), config_predicate("C2"), n_chains=c.chains, steps=c.steps,
+                 burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch)
+
+
+@pytest.mark.parametrize("key", ["C3", "C4", "C5"])
+def test_large_configs_sampled_chains(pbn, key):
+    """Full launch (bench.py's configuration); oracle on sampled chains."""
+    c = CONFIGS[key]
+    model, pred = config_model(key), config_predicate(key)
+    n_chains = c.chains
+    steps, burn_in = c.steps, c.burn_in
+    pm = load(pbn, model)
+    g = gpu_run(pm, model, pred, n_chains=n_chains, steps=steps, burn_in=burn_in, seed=c.sim_seed,
+                batch=c.batch)
+    ids = sample_chain_ids(n_chains, k=8, seed=c.sim_seed)
+    st, I, ws = oracle_run(model, pred, ids, steps=steps, burn_in=burn_in, seed=c.sim_seed,
+                           batch=c.batch, threads=8)
+    packed = pack_states(st)
+    for k, cid in enumerate(ids):
+        compare_chain(g, cid, packed[k], ws[k], steps, c.batch)
+    # properties that must hold for every chain at any size
+    c1 = g["c1"].astype(np.int64)
+    fl = g["first_last"].astype(np.int64)
+    first, last = fl & 1, fl >> 1
+    assert np.array_equal(g["n01"].astype(np.int64) - g["n10"].astype(np.int64), last - first)
+    assert np.array_equal(g["batch_sums"].astype(np.int64).sum(axis=1), c1)
+    pop = np.unpackbits(g["bits"].view(np.uint8), axis=1).sum(axis=1)
+    assert np.array_equal(pop, c1)
+    tot = g["totals"].astype(object)
+    assert tot[0] == int(c1.sum()) and tot[1] == int((c1.astype(object) ** 2).sum())
+    assert tot[2] == int(g["n01"].astype(np.int64).sum()) and tot[3] == int(g["n10"].astype(np.int64).sum())
+    assert tot[5] == int((c1 - last).sum()) and tot[4] == int(((steps - c1) - (1 - last)).sum())
+
+
+def test_launch_shape_independence(pbn):
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = load(pbn, model)
+    ref = gpu_run(pm, model, pred, n_chains=200, steps=700, burn_in=300, seed=9, batch=64)
+    for groups, warps in [(1, 1), (1, 7), (2, 5), (4, 8), (3, 10), (1, 25)]:
+        g = gpu_run(pm, model, pred, n_chains=200, steps=700, burn_in=300, seed=9, batch=64,
+                    groups=groups, warps=warps)
+        for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]:
+            assert np.array_equal(g[k], ref[k]), (groups, warps, k)
+
+
+def test_chain_split_and_step_split(pbn):
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = load(pbn, model)
+    full = gpu_run(pm, model, pred, n_chains=100, steps=640, burn_in=0, seed=5, batch=0)
+    # chains 0..36 and 37..99 in separate calls (chain_base)
+    a = gpu_run(pm, model, pred, n_chains=37, steps=640, seed=5)
+    b = gpu_run(pm, model, pred, n_chains=63, chain_base=37, steps=640, seed=5)
+    for k in ["state", "c1", "n01", "n10", "first_last", "bits"]:
+        assert np.array_equal(np.concatenate([a[k], b[k]]), full[k]), k
+    # steps 0..300 then 301..640 continuing the state; bits appended at an offset
+    s1 = gpu_run(pm, model, pred, n_chains=100, steps=300, seed=5, bits_row_words=20)
+    s2 = gpu_run(pm, model, pred, n_chains=100, steps=340, step0=300, seed=5, init=False,
+                 state=s1["state"], bits_offset=300, bits_row_words=20, bits_init=s1["bits"])
+    assert np.array_equal(s2["state"], full["state"])
+    assert np.array_equal(s2["bits"][:, :20], full["bits"][:, :20])
+    assert np.array_equal(s1["c1"].astype(np.int64) + s2["c1"], full["c1"])
+
+
+def edge_models():
+    rng = np.random.default_rng(0)
+    yield "n1_identity", model_from_lists(1, 0.3, [[([0], [0, 1], 1.0)]]), Predicate(
+        np.array([0], np.uint16), np.array([1], np.uint8))
+    yield "n5_ragged_quads", random_pbn(5, 1, 3, 0, 4, 0.05, seed=1), Predicate(
+        np.array([4], np.uint16), np.array([0], np.uint8))
+    yield "wide_ell_8", random_pbn(40, 5, 8, 1, 4, 0.01, seed=2), Predicate(
+        np.array([0, 39], np.uint16), np.array([1, 1], np.uint8))
+    yield "deep_theta_10", random_pbn(64, 1, 3, 6, 10, 0.002, seed=3), Predicate(
+        np.array([1, 2, 3], np.uint16), np.array([0, 1, 0], np.uint8))
+    yield "const_functions", random_pbn(37, 1, 4, 0, 1, 0.02, seed=4), Predicate(
+        np.zeros(0, np.uint16), np.zeros(0, np.uint8))
+    yield "heavy_perturbation", random_pbn(70, 1, 3, 1, 5, 0.3, seed=5), Predicate(
+        np.array([69], np.uint16), np.array([1], np.uint8))
+    nodes = []
+    for i in range(33):
+        nodes.append([([int(x) for x in rng.choice(33, 3, replace=False)],
+                       [int(b) for b in rng.integers(0, 2, 8)], 1.0)])
+    yield "boolean_network_ell1", model_from_lists(33, 1e-3, nodes), Predicate(
+        np.array([0], np.uint16), np.array([1], np.uint8))
+
+
+@pytest.mark.parametrize("per_node", [False, True])
+@pytest.mark.parametrize("name,model,pred", list(edge_models()), ids=[e[0] for e in edge_models()])
+def test_edge_models(pbn, name, model, pred, per_node):
+    full_compare(pbn, model, pred, n_chains=45, steps=777, burn_in=123, seed=17, batch=50,
+                 per_node=per_node)
+
+
+def test_edge_sizes(pbn):
+    model, pred = config_model("C1"), config_predicate("C1")
+    # steps = 0 (burn-in only), one chain, batch larger than the window
+    full_compare(pbn, model, pred, n_chains=1, steps=0, burn_in=50, seed=3)
+    full_compare(pbn, model, pred, n_chains=1, steps=1, burn_in=0, seed=3, batch=7)
+    full_compare(pbn, model, pred, n_chains=3, steps=31, burn_in=1, seed=3, batch=100)
+    full_compare(pbn, model, pred, n_chains=64, steps=33, burn_in=0, seed=3, batch=32)
+
+
+def test_recount_matches_oracle_subwindows(pbn):
+    import torch
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = load(pbn, model)
+    steps = 1500
+    g = gpu_run(pm, model, pred, n_chains=70, steps=steps, burn_in=10, seed=4)
+    _, I, _ = oracle_run(model, pred, np.arange(70), steps=steps, burn_in=10, seed=4)
+    bits = torch.from_numpy(g["bits"].view(np.int32)).cuda()
+    row = g["bits"].shape[1]
+    for start, length, batch in [(0, steps, 100), (37, 1000, 33), (1400, 100, 7), (5, 0, 0), (64, 1, 1)]:
+        c1 = torch.empty(70, dtype=torch.int32, device="cuda")
+        n01, n10 = torch.empty_like(c1), torch.empty_like(c1)
+        fl = torch.empty(70, dtype=torch.uint8, device="cuda")
+        nb = (length + batch - 1) // batch if batch else 0
+        bs = torch.empty((70, max(nb, 1)), dtype=torch.int32, device="cuda") if batch else None
+        tot = torch.empty(6, dtype=torch.int64, device="cuda")
+        pbn.pbn_recount(bits, 70, row, start, length, batch, c1, n01, n10, fl, bs, tot)
+        torch.cuda.synchronize()
+        ws = [ostats.window_stats(I[c, start:start + length], batch if batch else 1) for c in range(70)]
+        assert np.array_equal(c1.cpu().numpy(), [w.c1 for w in ws])
+        assert np.array_equal(n01.cpu().numpy(), [w.n01 for w in ws])
+        assert np.array_equal(n10.cpu().numpy(), [w.n10 for w in ws])
+        if length:
+            assert np.array_equal(fl.cpu().numpy(), [w.first | (w.last << 1) for w in ws])
+        if batch:
+            assert np.array_equal(bs.cpu().numpy()[:, :nb], np.stack([w.batch_sums for w in ws]))
+        assert np.array_equal(tot.cpu().numpy().view(np.uint64), ostats.totals(ws))
