@@ -169,75 +169,126 @@ pbn_status check_device_limits(const pbn_model_desc* d, char* err, size_t errlen
 }
 
 // Device image (layout: pbn_internal.h).
+struct ImageBuilder {
+    std::vector<uint8_t> buf;
+    uint32_t alloc(size_t bytes, size_t align = 16)
+    {
+        size_t off = (buf.size() + align - 1) & ~(align - 1);
+        buf.resize(off + bytes, 0);
+        return (uint32_t)off;
+    }
+    uint32_t* u32(uint32_t off) { return reinterpret_cast<uint32_t*>(buf.data() + off); }
+    uint16_t* u16(uint32_t off) { return reinterpret_cast<uint16_t*>(buf.data() + off); }
+};
+
+// Table entry idx of function f (parents[0] is the MSB of idx, reading Q5).
+inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
+{
+    return (d->tables[d->tbl_off[f] + (int32_t)(idx >> 5)] >> (idx & 31u)) & 1u;
+}
+
 std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
-    int32_t max_ell = 0, max_theta = 0;
-    int64_t aux_words = 0;
-    for (int32_t i = 0; i < n; ++i) max_ell = std::max(max_ell, d->fn_off[i + 1] - d->fn_off[i]);
-    for (int32_t f = 0; f < nf; ++f) {
-        const int32_t theta = d->par_off[f + 1] - d->par_off[f];
-        max_theta = std::max(max_theta, theta);
-        aux_words += (theta + 1) / 2;
-        if (theta >= 6) aux_words += ((int64_t)1 << theta) / 32;
+    ImageBuilder B;
+    std::vector<uint32_t> reloc;  // byte offsets of offset-valued words
+    const uint32_t off_nrec = B.alloc(16u * (size_t)n);
+    std::vector<int32_t> thmax(n, 0);
+    std::vector<char> fast(n, 0);
+    int32_t max_ell = 0, max_theta = 0, slow = 0, FT = pbn::kFastMinTheta;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t ell = d->fn_off[i + 1] - d->fn_off[i];
+        max_ell = std::max(max_ell, ell);
+        for (int32_t f = d->fn_off[i]; f < d->fn_off[i + 1]; ++f)
+            thmax[i] = std::max(thmax[i], d->par_off[f + 1] - d->par_off[f]);
+        max_theta = std::max(max_theta, thmax[i]);
+        fast[i] = ell <= pbn::kFastMaxEll && thmax[i] <= pbn::kFastMaxTheta;
+        slow += !fast[i];
+        if (fast[i]) FT = std::max(FT, thmax[i]);
     }
-    aux_words += 4;  // slack: reads never leave the section
     L->n = n;
     L->nf = nf;
-    L->aux_words = (int32_t)aux_words;
-    L->has_xthr = max_ell > 4;
     L->max_theta = max_theta;
     L->max_ell = max_ell;
-    L->off_nrec = 0;
-    L->off_fdesc = align16(L->off_nrec + 16u * n);
-    L->off_aux = align16(L->off_fdesc + 8u * nf);
-    L->off_xthr = align16(L->off_aux + 4u * (uint32_t)aux_words);
-    L->bytes = align16(L->off_xthr + (L->has_xthr ? 4u * nf : 0u));
+    L->slow_nodes = slow;
+    L->fast_theta = FT;
 
-    std::vector<uint8_t> img(L->bytes, 0);
-    uint32_t* nrec = reinterpret_cast<uint32_t*>(img.data() + L->off_nrec);
-    uint32_t* fdesc = reinterpret_cast<uint32_t*>(img.data() + L->off_fdesc);
-    uint32_t* aux = reinterpret_cast<uint32_t*>(img.data() + L->off_aux);
-    uint32_t* xthr = reinterpret_cast<uint32_t*>(img.data() + L->off_xthr);
-    uint32_t ap = 0;  // aux cursor (u32)
     for (int32_t i = 0; i < n; ++i) {
-        const int32_t f0 = d->fn_off[i], f1 = d->fn_off[i + 1];
-        const int32_t ell = f1 - f0;
-        uint32_t E[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+        const int32_t f0 = d->fn_off[i], f1 = d->fn_off[i + 1], ell = f1 - f0;
+        // selection thresholds E_1..E_{ell-1} (reading Q3)
+        std::vector<uint32_t> E;
         double cum = 0.0;
-        int32_t thmax = 0;
-        for (int32_t j = 0; j < ell; ++j) {
-            const int32_t f = f0 + j;
-            cum += d->sel_prob[f];
-            if (j < ell - 1) {
-                const uint32_t e = boundary_E(cum, Tp);
-                if (j < 3) E[j] = e;
-                if (L->has_xthr) xthr[f] = e;  // xthr[fn_base + k - 1] = E_k
-            }
-            const int32_t theta = d->par_off[f + 1] - d->par_off[f];
-            thmax = std::max(thmax, theta);
-            // descriptor
-            uint32_t t0 = 0;
-            if (theta <= 5) t0 = d->tables[d->tbl_off[f]];
-            fdesc[2 * f + 0] = t0;
-            fdesc[2 * f + 1] = (uint32_t)theta | (ap << 5);
-            // parents reversed: half-word m = parents[theta-1-m] as byte offset
-            uint16_t* h = reinterpret_cast<uint16_t*>(aux + ap);
-            for (int32_t m = 0; m < theta; ++m)
-                h[m] = (uint16_t)(4u * d->parents[d->par_off[f] + theta - 1 - m]);
-            ap += (uint32_t)(theta + 1) / 2;
-            if (theta >= 6) {
-                const int32_t words = (1 << theta) / 32;
-                for (int32_t w = 0; w < words; ++w) aux[ap + w] = d->tables[d->tbl_off[f] + w];
-                ap += (uint32_t)words;
-            }
+        for (int32_t j = 0; j + 1 < ell; ++j) {
+            cum += d->sel_prob[f0 + j];
+            E.push_back(boundary_E(cum, Tp));
         }
-        nrec[4 * i + 0] = E[0];
-        nrec[4 * i + 1] = E[1];
-        nrec[4 * i + 2] = E[2];
-        nrec[4 * i + 3] = (uint32_t)f0 | ((uint32_t)thmax << 20) | ((uint32_t)(ell - 1) << 25);
+        uint32_t w3 = 0;  // nrec[i].w, written last (B.alloc may move the buffer)
+        if (fast[i]) {
+            const uint32_t off_desc = B.alloc(16u * ell);
+            for (int32_t j = 0; j < ell; ++j) {
+                const int32_t f = f0 + j;
+                const int32_t theta = d->par_off[f + 1] - d->par_off[f];
+                // table padded to FT index bits: dummy parents are the low bits
+                uint64_t T = 0;
+                for (uint32_t idx = 0; idx < (1u << FT); ++idx)
+                    T |= (uint64_t)table_bit(d, f, idx >> (FT - theta)) << idx;
+                // padded parent list, MSB first; dummies read node 0
+                const uint32_t off_par = B.alloc(2u * (size_t)FT, 4);
+                uint16_t* par = B.u16(off_par);
+                for (int32_t m = 0; m < FT; ++m)
+                    par[m] = (uint16_t)(m < theta ? 4u * d->parents[d->par_off[f] + m] : 0u);
+                uint32_t* desc = B.u32(off_desc + 16u * j);
+                desc[0] = (uint32_t)T;
+                desc[1] = (uint32_t)(T >> 32);
+                desc[2] = off_par;
+                desc[3] = 0;
+                reloc.push_back(off_desc + 16u * j + 8u);
+            }
+            w3 = off_desc;
+        } else {
+            const uint32_t off_slow = B.alloc(16);
+            const uint32_t off_thr = B.alloc(4u * std::max<size_t>(E.size(), 1), 4);
+            for (size_t k = 0; k < E.size(); ++k) B.u32(off_thr)[k] = E[k];
+            const uint32_t off_gd = B.alloc(16u * ell);
+            for (int32_t j = 0; j < ell; ++j) {
+                const int32_t f = f0 + j;
+                const int32_t theta = d->par_off[f + 1] - d->par_off[f];
+                const int32_t words = d->tbl_off[f + 1] - d->tbl_off[f];
+                const uint32_t off_t = B.alloc(4u * words, 4);
+                for (int32_t w = 0; w < words; ++w) B.u32(off_t)[w] = d->tables[d->tbl_off[f] + w];
+                const uint32_t off_p = B.alloc(2u * (size_t)std::max(theta, 1), 4);
+                for (int32_t m = 0; m < theta; ++m)
+                    B.u16(off_p)[m] = (uint16_t)(4u * d->parents[d->par_off[f] + m]);
+                uint32_t* gd = B.u32(off_gd + 16u * j);
+                gd[0] = off_t;
+                gd[1] = (uint32_t)theta;
+                gd[2] = off_p;
+                gd[3] = 0;
+                reloc.push_back(off_gd + 16u * j);
+                reloc.push_back(off_gd + 16u * j + 8u);
+            }
+            uint32_t* sr = B.u32(off_slow);
+            sr[0] = off_thr;
+            sr[1] = (uint32_t)ell;
+            sr[2] = off_gd;
+            sr[3] = 0;
+            reloc.push_back(off_slow);
+            reloc.push_back(off_slow + 8u);
+            w3 = off_slow | pbn::kSlowFlag;
+        }
+        uint32_t* rec = B.u32(off_nrec + 16u * i);
+        for (int k = 0; k < 3; ++k) rec[k] = k < (int)E.size() ? E[k] : 0xFFFFFFFFu;
+        rec[3] = w3;
+        reloc.push_back(off_nrec + 16u * i + 12u);
     }
-    return img;
+    B.alloc(16);  // tail slack
+    L->bytes = (uint32_t)B.buf.size();
+    // relocation list after the image (not staged to shared memory)
+    L->reloc_off = B.alloc(4u * std::max<size_t>(reloc.size(), 1), 16);
+    L->reloc_count = (int32_t)reloc.size();
+    std::memcpy(B.buf.data() + L->reloc_off, reloc.data(), 4u * reloc.size());
+    B.alloc(16);
+    return B.buf;
 }
 
 pbn_status cuda_status(cudaError_t e, char* err, size_t errlen, const char* what)
@@ -339,6 +390,7 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     if (a->steps > 0 && a->batch > 0 && !o->batch_sums) return PBN_E_USAGE;
     if (a->steps > 0 && a->emit_bits && !o->bits) return PBN_E_USAGE;
     if (a->bits_offset < 0 || a->bits_row_words < 0) return PBN_E_USAGE;
+    if (a->groups_per_cta > 1) return PBN_E_USAGE;  // one 32-chain group per CTA
     std::memset(P, 0, sizeof(*P));
     P->image = m->d_image;
     P->L = m->L;
@@ -348,8 +400,12 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     P->nquads = (m->L.n + 3) / 4;
     P->n_pad = (m->L.n + 3) & ~3;
     P->state_words = (m->L.n + 31) / 32;
-    P->group_stride = (P->per_node ? 2 : 3) * P->n_pad + 32;
-    P->seed = a->seed;
+    P->group_words = (P->per_node ? 2 : 3) * P->n_pad + 32;
+    // Philox4x32-10 key schedule: round r uses (k0 + r W0, k1 + r W1), key = seed
+    for (uint32_t r = 0; r < 10; ++r) {
+        P->rk[2 * r + 0] = (uint32_t)a->seed + r * 0x9E3779B9u;
+        P->rk[2 * r + 1] = (uint32_t)(a->seed >> 32) + r * 0xBB67AE85u;
+    }
     P->n_chains = a->n_chains;
     P->chain_base = a->chain_base;
     P->step0 = a->step0;
@@ -392,7 +448,7 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     if (a->n_chains == 0) return PBN_OK;
     pbn::LaunchPlan plan;
     const char* why = nullptr;
-    int rc = pbn::plan_traj_launch(P, m->device, a->groups_per_cta, a->warps_per_group, &plan, &why);
+    int rc = pbn::plan_traj_launch(P, m->device, a->warps_per_group, &plan, &why);
     if (rc < 0) return PBN_E_USAGE;
     if (rc > 0) return PBN_E_CUDA;
     rc = pbn::launch_traj(P, plan, stream);

@@ -1,26 +1,37 @@
 // pbn_internal.h -- internal layout shared by the host API (pbn_api.cpp) and
 // the kernels (pbn_traj.cu, pbn_recount.cu).  Not part of the C ABI.
 //
-// Device image of a PBN (built once by pbn_load).  One
-// contiguous blob, 16-byte aligned sections, staged whole into each CTA's
-// shared memory with one bulk async copy when it fits:
+// Device image of a PBN (built once by pbn_load): one
+// contiguous blob addressed by BYTE OFFSETS from its start, every record
+// 16-byte aligned, staged whole into each CTA's shared memory with a bulk
+// async copy when it fits (else read through the read-only global path).
 //
-//   nrec [n]    uint4 per node i:
-//                 .x .y .z  selection thresholds E_1..E_3 of node i, where
-//                           function j (0-based) is chosen iff
-//                           j = #{k : u > E_k} (E_k = D_k - 1, reading Q3);
-//                           unused entries are 0xFFFFFFFF
-//                 .w        fn_base (bits 0-19) | theta_max of the node
-//                           (bits 20-24) | ell-1 (bits 25-31)
-//   fdesc[nf]   uint2 per function f:
-//                 .x        truth table word 0 (theta <= 5: the whole table)
-//                 .y        theta (bits 0-4) | aux offset in u32 (bits 5-31)
-//   aux  []     per function: ceil(theta/2) u32 holding theta u16 parent
-//               byte offsets (node * 4) in REVERSED order -- half-word m is
-//               parents[theta-1-m], i.e. the parent whose bit is index bit m
-//               (parents[0] is the MSB, reading Q5); then, for theta >= 6,
-//               the 2^theta/32 table words.
-//   xthr [nf]   only when some ell(i) > 4: xthr[fn_base + k - 1] = E_k
+//   nrec[i] (uint4, node i)       {E1, E2, E3, w}
+//       E_k  selection thresholds of reading Q3 as E_k = D_k - 1: the
+//            selected function is j = #{k : u > E_k}; unused = 0xFFFFFFFF
+//       w    FAST node (ell <= 4, theta_max <= 6): offset of the node's first
+//            fast descriptor (16-aligned, low bits 0)
+//            SLOW node (anything else): offset of its slow record | 1
+//   fast descriptor (uint4, per function of a fast node)   {t0, t1, plist, 0}
+//       every fast function is PADDED to the model-wide fast width FT (the
+//       largest theta over fast nodes, 3 <= FT <= 6): its parent list is
+//       extended with dummy parents that the table ignores
+//       (table'[idx'] = table[idx' >> (FT - theta)]), so every lane of a warp
+//       gathers exactly FT parents whatever function it chose -- the gather is
+//       straight-line code with a compile-time trip count.
+//       t0,t1  the padded 2^FT-entry table (entries 0-31 in t0, 32-63 in t1)
+//       plist  offset of the padded parent list: FT u16 entries holding
+//              (parent node * 4), MSB first (parents[0] first, reading Q5)
+//   slow record (uint4, per slow node)  {thr, ell, gdesc, 0}
+//       thr    offset of ell-1 u32 thresholds E_1..E_{ell-1}
+//       gdesc  offset of ell generic descriptors
+//   generic descriptor (uint4)          {toff, theta, poff, 0}
+//       toff   offset of the ceil(2^theta/32) table words; poff: u16 parent list
+//              (node*4), parents[0] first (MSB, reading Q5)
+//   relocation list (u32, stored after the image in device memory, not staged)
+//       byte offsets of every offset-valued word above (nrec.w, plist, thr,
+//       gdesc, toff, poff).  After staging, each CTA adds its shared-memory
+//       base to those words, so the hot loop uses absolute shared addresses.
 //
 // The thresholds are the product's own computation of reading Q3
 // (pbn_api.cpp build_image); nothing here is shared with oracle/.
@@ -31,30 +42,34 @@ namespace pbn {
 
 constexpr int kMaxPred = 16;
 constexpr int kMaxWarpsPerCta = 32;
+constexpr uint32_t kSlowFlag = 1;
+constexpr int kFastMaxTheta = 6;
+constexpr int kFastMinTheta = 3;
+constexpr int kFastMaxEll = 4;
 
 struct ImageLayout {
-    uint32_t off_nrec = 0, off_fdesc = 0, off_aux = 0, off_xthr = 0;
-    uint32_t bytes = 0;
+    uint32_t bytes = 0;        // image bytes (staged to shared memory)
+    uint32_t reloc_off = 0;    // byte offset of the relocation list after the image
+    int32_t reloc_count = 0;
     int32_t n = 0, nf = 0;
-    int32_t aux_words = 0;
-    int32_t has_xthr = 0;
     int32_t max_theta = 0, max_ell = 0;
+    int32_t slow_nodes = 0;
+    int32_t fast_theta = kFastMinTheta;  // FT
 };
 
 struct TrajParams {
-    const uint8_t* image;      // device image (global)
+    const uint8_t* image;      // device image (global); relocation list at image + L.reloc_off
     ImageLayout L;
+    uint32_t rk[20];           // Philox round keys (k0 + r W0, k1 + r W1), r = 0..9
     uint32_t Tp;
     int32_t per_node;          // PBN_PERTURB_PER_NODE semantics
     int32_t n;
     int32_t nquads;            // ceil(n/4)
     int32_t n_pad;             // n rounded up to a multiple of 4 (u32 words per buffer)
     int32_t state_words;       // ceil(n/32): row stride of the chain-major state
-    int32_t groups_per_cta;
-    int32_t warps_per_group;
-    int32_t group_stride;      // u32 words of shared memory per chain group
+    int32_t warps_per_group;   // one 32-chain group per CTA
+    int32_t group_words;       // u32 words of shared memory for the group's state
     uint32_t image_smem_bytes; // 0 when the image is read from global memory
-    uint64_t seed;
     int64_t n_chains, chain_base, step0, burn_in, steps, batch;
     int32_t init, emit_bits;
     int32_t pred_k;
@@ -75,7 +90,6 @@ struct TrajParams {
 };
 
 struct LaunchPlan {
-    int groups_per_cta;
     int warps_per_group;
     int ctas;
     int threads;
@@ -83,10 +97,9 @@ struct LaunchPlan {
     bool image_in_smem;
 };
 
-// Implemented in pbn_traj.cu.  Returns 0 on success, else a cudaError_t value;
-// *usage_error set (and nonzero returned) when the sizes cannot be served.
-int plan_traj_launch(const TrajParams& P, int device, int want_groups, int want_warps,
-                     LaunchPlan* plan, const char** why);
+// Implemented in pbn_traj.cu.  Returns 0 on success, a cudaError_t value on a
+// CUDA failure, or -1 (with *why set) when the sizes cannot be served.
+int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why);
 int launch_traj(TrajParams P, const LaunchPlan& plan, void* stream);
 
 struct RecountParams {

@@ -8,27 +8,33 @@
 //              group's 32 chains (bit l = lane l), double-buffered (A7).  A
 //              group's nodes are split over W warps (4-node quads, the Philox
 //              granularity); a named barrier per group closes each step.
-//   per node   the warp walks its nodes in lock-step, so all network metadata
-//              reads are broadcasts; per lane: one 32-bit Philox word u (A3),
-//              perturbation u < T_p (A4), function j = #{k : u > E_k} (A5),
-//              parent bits gathered from the old buffer with a rotate so bit
-//              `lane` lands at index position m (A6), table lookup, and one
-//              __ballot_sync commits the 32 chains' new bits as one word (A7).
+//   per node   the warp walks its nodes in lock-step, so network metadata reads
+//              are broadcasts (<= 4 distinct addresses); per lane: one 32-bit
+//              Philox word u (A3), perturbation u < T_p (A4), function
+//              j = #{k : u > E_k} (A5), then the node's theta_max parents are
+//              gathered MSB-first -- every function of a node is padded to the
+//              node's theta_max (pbn_internal.h), so the gather count is
+//              warp-uniform and branch-free: per parent one LDS of the parent
+//              word, a rotate that brings bit `lane` to bit 31 and a funnel
+//              shift that appends it to the index (A6); the padded 64-bit table
+//              gives the bit and one __ballot_sync commits the 32 chains' new
+//              bits as one word (A7).
 //   VECTOR each step also stores gamma words; after the
 //              step barrier every warp patches its own nodes for the chains
 //              with any gamma: new = (f & ~M) | ((old ^ gamma) & M).
 //   stats      warp 0 of each group evaluates the property on the new words
 //              (A8: AND over (node, value) pairs, bit-sliced) and keeps per
 //              lane (= chain) counters in registers: c1, n01, n10, first/last,
-//              batch sums, packed bits (A9); epilogue writes them and adds the
-//              six u64 totals with integer atomics (A10, order-independent).
-//   image      the model image is staged into shared memory once per CTA with
-//              one cp.async.bulk (TMA bulk copy, mbarrier completion) when it
-//              fits; otherwise it is read through the read-only L1 path.
+//              batch sums, packed bits (A9); the epilogue writes them and adds
+//              the six u64 totals with integer atomics (A10, order-independent).
+//   image      staged into shared memory once per CTA by cp.async.bulk (TMA
+//              bulk copy, mbarrier completion) when it fits; otherwise read
+//              through the read-only global path (ld.global.nc).
 //
 // Randomness: Philox4x32-10 with counter (i/4, chain, t lo, t hi) and key
-// (seed lo, seed hi) -- reading Q2.  Every output depends only on (model,
-// seed, chain id, absolute step), never on the launch shape.
+// (seed lo, seed hi) -- reading Q2; the round keys are precomputed on the
+// host and read from the constant bank.  Every output depends only on
+// (model, seed, chain id, absolute step), never on the launch shape.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,127 +49,171 @@ namespace {
 
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
-// Philox4x32-10 (Salmon et al., SC'11), product implementation.
+__device__ __forceinline__ void mulhilo(uint32_t a, uint32_t m, uint32_t& lo, uint32_t& hi)
+{
+    asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}"
+        : "=r"(lo), "=r"(hi)
+        : "r"(a), "r"(m));
+}
+
+// Philox4x32-10 (Salmon et al., SC'11) with precomputed round keys.
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                               uint32_t k0, uint32_t k1)
+                                               const uint32_t* __restrict__ rk)
 {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
-        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
-        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
-        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
-        c1 = (uint32_t)p1;
-        c3 = (uint32_t)p0;
+        uint32_t lo0, hi0, lo1, hi1;
+        mulhilo(c0, 0xD2511F53u, lo0, hi0);
+        mulhilo(c2, 0xCD9E8D57u, lo1, hi1);
+        const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r];
+        const uint32_t n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+        c1 = lo1;
+        c3 = lo0;
         c0 = n0;
         c2 = n2;
-        k0 += 0x9E3779B9u;
-        k1 += 0xBB67AE85u;
     }
     return make_uint4(c0, c1, c2, c3);
 }
 
-__device__ __forceinline__ void group_barrier(int id, int nthreads)
-{
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
 {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// Image accessors: shared memory (SMEM=true) or read-only global path.
-template <bool SMEM>
-struct Img {
-    const uint4* nrec;
-    const uint2* fdesc;
-    const uint32_t* aux;
-    const uint32_t* xthr;
-    __device__ __forceinline__ uint4 rec(int i) const { return SMEM ? nrec[i] : __ldg(nrec + i); }
-    __device__ __forceinline__ uint2 desc(uint32_t f) const { return SMEM ? fdesc[f] : __ldg(fdesc + f); }
-    __device__ __forceinline__ uint32_t a32(uint32_t w) const { return SMEM ? aux[w] : __ldg(aux + w); }
-    __device__ __forceinline__ uint32_t a16(uint32_t h) const
-    {
-        const uint16_t* p = reinterpret_cast<const uint16_t*>(aux) + h;
-        return SMEM ? (uint32_t)*p : (uint32_t)__ldg(p);
-    }
-    __device__ __forceinline__ uint32_t xt(uint32_t f) const { return SMEM ? xthr[f] : __ldg(xthr + f); }
-};
-
-// One node of one step for the warp's 32 chains (A4-A7).
-template <bool SMEM, bool PER_NODE>
-__device__ __forceinline__ void step_node(const Img<SMEM>& img, int i, uint32_t u, uint32_t Tp,
-                                          const uint32_t* __restrict__ old, uint32_t* __restrict__ nw,
-                                          uint32_t* __restrict__ gam, uint32_t& any, int lane)
+// shared-memory accessors on 32-bit shared addresses.  State words change
+// every step (volatile: never cached across barriers); image words are
+// immutable (plain asm: the compiler may schedule and CSE them freely).
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
 {
-    const uint4 rec = img.rec(i);
-    const bool flip = u < Tp;                                   // gamma_i(t) = 1 (A4)
-    const uint32_t gw = __ballot_sync(FULL, flip);
-    const uint32_t fn_base = rec.w & 0xFFFFFu;
-    const uint32_t thmax = (rec.w >> 20) & 31u;
-    const uint32_t ellm1 = rec.w >> 25;
-    // function selection by the same word (A5): j = #{k : u > E_k}
-    uint32_t j = (uint32_t)(u > rec.x) + (uint32_t)(u > rec.y) + (uint32_t)(u > rec.z);
-    if (ellm1 > 3u) {
-        for (uint32_t k = 3; k < ellm1; ++k) j += (uint32_t)(u > img.xt(fn_base + k));
-    }
-    const uint2 d = img.desc(fn_base + j);
-    const uint32_t theta = d.y & 31u;
-    const uint32_t auxo = d.y >> 5;
-    // parent gather (A6): parent m's bit for this lane lands at index bit m
-    uint32_t idx = 0;
-    for (uint32_t m = 0; m < thmax; ++m) {
-        if (m < theta) {
-            const uint32_t off = img.a16(2u * auxo + m);
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(
-                reinterpret_cast<const uint8_t*>(old) + off);
-            idx |= __funnelshift_r(w, w, (uint32_t)lane - m) & (1u << m);
-        }
-    }
-    uint32_t tw;
-    if (theta <= 5u) {
-        tw = d.x;
-    } else {
-        tw = img.a32(auxo + ((theta + 1u) >> 1) + (idx >> 5));
-    }
-    const bool bit = (tw >> (idx & 31u)) & 1u;
-    uint32_t nb = __ballot_sync(FULL, bit);                     // commit (A7)
-    if (PER_NODE) {
-        const uint32_t ow = old[i];
-        nb = (nb & ~gw) | (~ow & gw);
-    } else {
-        any |= gw;
-    }
-    if (lane == 0) {
-        nw[i] = nb;
-        if (!PER_NODE) gam[i] = gw;
-    }
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32_ro(uint32_t a)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds16_ro(uint32_t a)
+{
+    uint16_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return (uint32_t)v;
+}
+__device__ __forceinline__ uint4 lds128_ro(uint32_t a)
+{
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-template <bool SMEM, bool PER_NODE>
+
+// Image accessors.  SMEM: the staged image was relocated, so every stored
+// offset is already an absolute shared address.  Global: offsets are
+// relative to the image pointer (read-only path).
+template <bool SMEM>
+struct Img {
+    const uint8_t* gbase;  // global address of the image (!SMEM)
+    __device__ __forceinline__ uint4 ld128(uint32_t a) const
+    {
+        if (SMEM) return lds128_ro(a);
+        return __ldg(reinterpret_cast<const uint4*>(gbase + a));
+    }
+    __device__ __forceinline__ uint32_t ld32(uint32_t a) const
+    {
+        if (SMEM) return lds32_ro(a);
+        return __ldg(reinterpret_cast<const uint32_t*>(gbase + a));
+    }
+    __device__ __forceinline__ uint32_t ld16(uint32_t a) const
+    {
+        if (SMEM) return lds16_ro(a);
+        return (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(gbase + a));
+    }
+};
+
+// Generic path for nodes outside the fast shape (ell > 4 or theta_max > 6).
+template <bool SMEM>
+__device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w, uint32_t u, uint32_t old,
+                                               uint32_t rot)
+{
+    const uint4 sr = img.ld128(w & ~15u);  // {thr, ell, gdesc, 0}
+    uint32_t j = 0;
+    for (uint32_t k = 0; k + 1 < sr.y; ++k) j += (uint32_t)(u > img.ld32(sr.x + 4u * k));
+    const uint4 gd = img.ld128(sr.z + 16u * j);  // {toff, theta, poff, 0}
+    uint32_t idx = 0;
+    for (uint32_t m = 0; m < gd.y; ++m) {
+        const uint32_t off = img.ld16(gd.z + 2u * m);
+        const uint32_t wv = lds32(old + off);
+        idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+    }
+    const uint32_t tw = img.ld32(gd.x + 4u * (idx >> 5));
+    return (tw >> (idx & 31u)) & 1u;
+}
+
+// One node of one step for the warp's 32 chains (A4-A7).  Returns the gamma word.
+template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
+__device__ __forceinline__ uint32_t step_node(const Img<SMEM>& img, uint32_t rec_addr, uint32_t i, uint32_t u,
+                                              uint32_t Tp, uint32_t old, uint32_t nw, uint32_t gam, uint32_t rot,
+                                              bool leader)
+{
+    const uint4 rec = img.ld128(rec_addr);
+    const uint32_t gw = __ballot_sync(FULL, u < Tp);  // gamma_i(t) = 1 (A4)
+    uint32_t bit;
+    if (!SLOW || !(rec.w & kSlowFlag)) {
+        // A5: descriptor of function j = #{k : u > E_k}
+        uint32_t dp = rec.w;
+        if (u > rec.x) dp += 16u;
+        if (u > rec.y) dp += 16u;
+        if (u > rec.z) dp += 16u;
+        const uint4 d = img.ld128(dp);  // {t0, t1, plist, 0}
+        // A6: gather the FT padded parents, MSB first: rotate bit `lane` of the
+        // parent word to bit 31, funnel it into the index
+        uint32_t idx = 0;
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+            const uint32_t off = img.ld16(d.z + 2u * k);
+            const uint32_t wv = lds32(old + off);
+            idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+        }
+        const uint32_t tw = (FT == 6 && idx >= 32u) ? d.y : d.x;
+        bit = (tw >> (idx & 31u)) & 1u;
+    } else {
+        bit = slow_node_bit<SMEM>(img, rec.w, u, old, rot);
+    }
+    uint32_t nb = __ballot_sync(FULL, bit != 0u);  // commit (A7)
+    if (PER_NODE) {
+        const uint32_t ow = lds32(old + 4u * i);
+        nb = (nb & ~gw) | (~ow & gw);
+    }
+    if (leader) {
+        sts32(nw + 4u * i, nb);
+        if (!PER_NODE) sts32(gam + 4u * i, gw);
+    }
+    return gw;
+}
+
+template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
 __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ TrajParams P)
 {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
 
     const int tid = threadIdx.x;
-    const int warp = tid >> 5;
+    const int wg = tid >> 5;  // warp within the (single) group of this CTA
     const int lane = tid & 31;
     const int W = P.warps_per_group;
-    const int g = warp / W;
-    const int wg = warp - g * W;
     const int n = P.n;
+    const uint32_t sbase = smem_u32(smem);
 
-    // ---- A1: stage the model image into shared memory (one bulk copy) ----
+    // ---- A1: stage the model image into shared memory (bulk async copy) ----
     Img<SMEM> img;
-    {
-        const uint8_t* base = SMEM ? smem : P.image;
-        img.nrec = reinterpret_cast<const uint4*>(base + P.L.off_nrec);
-        img.fdesc = reinterpret_cast<const uint2*>(base + P.L.off_fdesc);
-        img.aux = reinterpret_cast<const uint32_t*>(base + P.L.off_aux);
-        img.xthr = reinterpret_cast<const uint32_t*>(base + P.L.off_xthr);
-    }
+    img.gbase = P.image;
     if (SMEM) {
         const uint32_t bar = smem_u32(&mbar);
         if (tid == 0) {
@@ -177,7 +227,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                 const uint32_t sz = min(chunk, P.image_smem_bytes - off);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-                    "[%3];" ::"r"(smem_u32(smem + off)),
+                    "[%3];" ::"r"(sbase + off),
                     "l"(P.image + off), "r"(sz), "r"(bar)
                     : "memory");
             }
@@ -188,37 +238,42 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
             "@!p bra WAIT_%=;\n}\n" ::"r"(bar)
             : "memory");
+        // relocate: offsets -> absolute shared addresses of this CTA's copy
+        const uint32_t* rel = reinterpret_cast<const uint32_t*>(P.image + P.L.reloc_off);
+        for (int k = tid; k < P.L.reloc_count; k += blockDim.x) {
+            const uint32_t a = sbase + __ldg(rel + k);
+            sts32(a, lds32(a) + sbase);
+        }
+        __syncthreads();
     }
 
-    const int64_t group = (int64_t)blockIdx.x * P.groups_per_cta + g;
-    if (g >= P.groups_per_cta || group * 32 >= P.n_chains) return;
-    const int64_t chain_local = group * 32 + lane;
+    const int64_t chain_local = (int64_t)blockIdx.x * 32 + lane;
     const bool valid = chain_local < P.n_chains;
     const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
+    const bool leader = lane == 0;
+    const uint32_t rot = 31u - (uint32_t)lane;  // rotate-left amount: bit `lane` -> bit 31
 
-    uint32_t* gbase = reinterpret_cast<uint32_t*>(smem + P.image_smem_bytes) + (size_t)g * P.group_stride;
-    uint32_t* bufA = gbase;                 // bufA: current state, bufB: next
-    uint32_t* bufB = gbase + P.n_pad;
-    uint32_t* gam = gbase + 2 * P.n_pad;                        // VECTOR only
-    uint32_t* anyw = gbase + (PER_NODE ? 2 : 3) * P.n_pad;      // [W]
-    const int bar_id = 1 + g;
-    const int bar_n = W * 32;
+    const uint32_t gbase = sbase + P.image_smem_bytes;
+    uint32_t bufA = gbase;                       // current state s_{t-1}
+    uint32_t bufB = gbase + 4u * P.n_pad;        // next state s_t
+    const uint32_t gam = gbase + 8u * P.n_pad;   // VECTOR: gamma words
+    const uint32_t anyw = gbase + 4u * (PER_NODE ? 2 : 3) * P.n_pad;  // [W]
+    const uint32_t nrec = SMEM ? sbase : 0u;     // node records start the image
 
     const int q0 = (int)((int64_t)wg * P.nquads / W);
     const int q1 = (int)((int64_t)(wg + 1) * P.nquads / W);
-    const uint32_t k0 = (uint32_t)P.seed, k1 = (uint32_t)(P.seed >> 32);
 
     // ---- A2: initial state ----
     if (P.init) {
         for (int q = q0; q < q1; ++q) {
-            const uint4 r = philox4x32_10((uint32_t)q, chain, 0u, 0u, k0, k1);
+            const uint4 r = philox4x32_10((uint32_t)q, chain, 0u, 0u, P.rk);
             const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int i = 4 * q + k;
                 if (i < n) {
                     const uint32_t wv = __ballot_sync(FULL, (rr[k] >> 31) != 0u);
-                    if (lane == 0) bufA[i] = wv;
+                    if (leader) sts32(bufA + 4u * i, wv);
                 }
             }
         }
@@ -231,55 +286,63 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                 const int i = 32 * b + k;
                 if (i >= n) break;
                 const uint32_t wv = __ballot_sync(FULL, (v >> k) & 1u);
-                if (lane == 0) bufA[i] = wv;
+                if (leader) sts32(bufA + 4u * i, wv);
             }
         }
     }
-    group_barrier(bar_id, bar_n);
+    __syncthreads();
 
-    // ---- per-lane statistics (warp 0 of the group) ----
+    // ---- per-lane statistics (warp 0) ----
     uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0;
     int64_t bcount = 0;  // elements in the current batch
     const int64_t total = P.burn_in + P.steps;
     const uint32_t Tp = P.Tp;
+    const bool full_quads = (n & 3) == 0 || q1 < P.nquads;  // this warp never sees a ragged quad
 
     for (int64_t r = 1; r <= total; ++r) {
         const uint64_t t = (uint64_t)(P.step0 + r);
         const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
-        const uint32_t* old = bufA;
-        uint32_t* nw = bufB;
         uint32_t any = 0;
         for (int q = q0; q < q1; ++q) {
-            const uint4 rw = philox4x32_10((uint32_t)q, chain, t_lo, t_hi, k0, k1);
-            const int i0 = 4 * q;
-            if (i0 + 3 < n) {
-                step_node<SMEM, PER_NODE>(img, i0 + 0, rw.x, Tp, old, nw, gam, any, lane);
-                step_node<SMEM, PER_NODE>(img, i0 + 1, rw.y, Tp, old, nw, gam, any, lane);
-                step_node<SMEM, PER_NODE>(img, i0 + 2, rw.z, Tp, old, nw, gam, any, lane);
-                step_node<SMEM, PER_NODE>(img, i0 + 3, rw.w, Tp, old, nw, gam, any, lane);
+            const uint4 rw = philox4x32_10((uint32_t)q, chain, t_lo, t_hi, P.rk);
+            const uint32_t i0 = 4u * (uint32_t)q;
+            const uint32_t ra = nrec + 16u * i0;
+            if (full_quads || q + 1 < P.nquads) {
+                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra, i0, rw.x, Tp, bufA, bufB, gam, rot, leader);
+                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u, i0 + 1, rw.y, Tp, bufA, bufB, gam, rot,
+                                                           leader);
+                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 32u, i0 + 2, rw.z, Tp, bufA, bufB, gam, rot,
+                                                           leader);
+                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 48u, i0 + 3, rw.w, Tp, bufA, bufB, gam, rot,
+                                                           leader);
             } else {
                 const uint32_t rr[4] = {rw.x, rw.y, rw.z, rw.w};
-                for (int k = 0; k < 4 && i0 + k < n; ++k)
-                    step_node<SMEM, PER_NODE>(img, i0 + k, rr[k], Tp, old, nw, gam, any, lane);
+                for (uint32_t k = 0; k < 4 && (int)(i0 + k) < n; ++k)
+                    any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u * k, i0 + k, rr[k], Tp, bufA, bufB, gam,
+                                                               rot, leader);
             }
         }
-        if (!PER_NODE && lane == 0) anyw[wg] = any;
-        group_barrier(bar_id, bar_n);
+        if (!PER_NODE && leader) sts32(anyw + 4u * wg, any);
+        __syncthreads();
         if (!PER_NODE) {
             // VECTOR: chains with any gamma take s XOR gamma instead of f(s)
             uint32_t M = 0;
-            for (int w = 0; w < W; ++w) M |= anyw[w];
+            for (int w = 0; w < W; ++w) M |= lds32(anyw + 4u * w);
             if (M) {
                 const int lo = 4 * q0, hi = min(4 * q1, n);
-                for (int i = lo + lane; i < hi; i += 32) nw[i] = (nw[i] & ~M) | ((old[i] ^ gam[i]) & M);
+                for (int i = lo + lane; i < hi; i += 32) {
+                    const uint32_t a = 4u * (uint32_t)i;
+                    const uint32_t f = lds32(bufB + a), o = lds32(bufA + a), gmm = lds32(gam + a);
+                    sts32(bufB + a, (f & ~M) | ((o ^ gmm) & M));
+                }
             }
-            group_barrier(bar_id, bar_n);
+            __syncthreads();
         }
         if (wg == 0 && r > P.burn_in) {
             // A8: property indicator, bit-sliced over the group's chains
             uint32_t Iw = FULL;
             for (int k = 0; k < P.pred_k; ++k) {
-                const uint32_t w = nw[P.pred_node[k]];
+                const uint32_t w = lds32(bufB + 4u * P.pred_node[k]);
                 Iw &= P.pred_val[k] ? w : ~w;
             }
             const uint32_t b = (Iw >> lane) & 1u;
@@ -318,12 +381,13 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                 }
             }
         }
-        { uint32_t* tmp = bufA; bufA = bufB; bufB = tmp; }  // bufA holds the newest state
+        const uint32_t tmp = bufA;  // bufA now holds the newest state
+        bufA = bufB;
+        bufB = tmp;
     }
 
     // ---- epilogue: final state back to chain-major rows ----
     {
-        const uint32_t* fin = bufA;
         const int nb = P.state_words;
         const int b0 = (int)((int64_t)wg * nb / W), b1 = (int)((int64_t)(wg + 1) * nb / W);
         for (int b = b0; b < b1; ++b) {
@@ -331,7 +395,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             for (int k = 0; k < 32; ++k) {
                 const int i = 32 * b + k;
                 if (i >= n) break;
-                v |= ((fin[i] >> lane) & 1u) << k;
+                v |= ((lds32(bufA + 4u * i) >> lane) & 1u) << k;
             }
             if (valid) P.state[chain_local * nb + b] = v;
         }
@@ -363,7 +427,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], o);
             }
-            if (lane == 0) {
+            if (leader) {
 #pragma unroll
                 for (int k = 0; k < 6; ++k)
                     if (v[k]) atomicAdd(P.totals + k, v[k]);
@@ -372,93 +436,68 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
     }
 }
 
-template <bool SMEM, bool PER_NODE>
-const void* kernel_ptr()
+// kernel table: [SMEM][PER_NODE][FT-3][SLOW]
+template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
+const void* kptr()
 {
-    return reinterpret_cast<const void*>(&traj_kernel<SMEM, PER_NODE>);
+    return reinterpret_cast<const void*>(&traj_kernel<SMEM, PER_NODE, FT, SLOW>);
 }
 
-int sm_count(int device)
+template <bool SMEM, bool PER_NODE>
+const void* pick_ft(int FT, bool slow)
 {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
-    return v;
+    switch (FT) {
+        case 3: return slow ? kptr<SMEM, PER_NODE, 3, true>() : kptr<SMEM, PER_NODE, 3, false>();
+        case 4: return slow ? kptr<SMEM, PER_NODE, 4, true>() : kptr<SMEM, PER_NODE, 4, false>();
+        case 5: return slow ? kptr<SMEM, PER_NODE, 5, true>() : kptr<SMEM, PER_NODE, 5, false>();
+        default: return slow ? kptr<SMEM, PER_NODE, 6, true>() : kptr<SMEM, PER_NODE, 6, false>();
+    }
+}
+
+const void* pick_kernel(bool smem, bool per_node, int FT, bool slow)
+{
+    if (smem) return per_node ? pick_ft<true, true>(FT, slow) : pick_ft<true, false>(FT, slow);
+    return per_node ? pick_ft<false, true>(FT, slow) : pick_ft<false, false>(FT, slow);
 }
 
 }  // namespace
 
-int plan_traj_launch(const TrajParams& P, int device, int want_groups, int want_warps,
-                     LaunchPlan* plan, const char** why)
+int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why)
 {
     int smem_optin = 0;
     cudaError_t e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e != cudaSuccess) return (int)e;
     const size_t static_smem = 64;  // mbarrier + slack
     const size_t limit = (size_t)smem_optin - static_smem;
-    const size_t group_bytes = (size_t)P.group_stride * 4;
-    const int64_t total_groups = (P.n_chains + 31) / 32;
-    const int sms = sm_count(device);
-
-    bool in_smem = (size_t)P.L.bytes + group_bytes <= limit;
+    const size_t group_bytes = (size_t)P.group_words * 4;
+    const bool in_smem = (size_t)P.L.bytes + group_bytes <= limit;
     const size_t img = in_smem ? P.L.bytes : 0;
     if (img + group_bytes > limit) {
         *why = "network too large: one 32-chain group's state does not fit in shared memory";
         return -1;
     }
-    const int g_fit = (int)((limit - img) / group_bytes);
-    int G;
-    if (want_groups > 0) {
-        G = want_groups;
-        if (G > g_fit) {
-            *why = "groups_per_cta exceeds what fits in shared memory";
-            return -1;
-        }
-    } else {
-        // spread groups so that every SM gets work before stacking groups
-        int64_t per_sm = (total_groups + sms - 1) / sms;
-        G = (int)std::min<int64_t>(std::max<int64_t>(per_sm, 1), g_fit);
-        G = std::min(G, kMaxWarpsPerCta);
-    }
-    int Wp;
-    if (want_warps > 0) {
-        Wp = want_warps;
-    } else {
-        Wp = kMaxWarpsPerCta / G;
-        Wp = std::max(1, std::min(Wp, P.nquads));
-    }
-    if (G * Wp > kMaxWarpsPerCta || Wp > P.nquads) {
-        *why = "groups_per_cta * warps_per_group must be <= 32 and warps_per_group <= ceil(n/4)";
+    int Wp = want_warps > 0 ? want_warps : std::max(1, std::min(kMaxWarpsPerCta, P.nquads));
+    if (Wp > kMaxWarpsPerCta || Wp > P.nquads) {
+        *why = "warps_per_group must be <= 32 and <= ceil(n/4)";
         return -1;
     }
-    if (G + 1 > 16) {
-        *why = "at most 15 groups per CTA (named barriers)";
-        return -1;
-    }
-    plan->groups_per_cta = G;
     plan->warps_per_group = Wp;
-    plan->ctas = (int)((total_groups + G - 1) / G);
-    plan->threads = G * Wp * 32;
-    plan->smem_bytes = img + (size_t)G * group_bytes;
+    plan->ctas = (int)((P.n_chains + 31) / 32);
+    plan->threads = Wp * 32;
+    plan->smem_bytes = img + group_bytes;
     plan->image_in_smem = in_smem;
     return 0;
 }
 
 int launch_traj(TrajParams P, const LaunchPlan& plan, void* stream)
 {
-    P.groups_per_cta = plan.groups_per_cta;
     P.warps_per_group = plan.warps_per_group;
     P.image_smem_bytes = plan.image_in_smem ? P.L.bytes : 0u;
-    const void* fn;
-    if (plan.image_in_smem)
-        fn = P.per_node ? kernel_ptr<true, true>() : kernel_ptr<true, false>();
-    else
-        fn = P.per_node ? kernel_ptr<false, true>() : kernel_ptr<false, false>();
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)plan.smem_bytes);
+    const void* fn = pick_kernel(plan.image_in_smem, P.per_node != 0, P.L.fast_theta, P.L.slow_nodes > 0);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
     if (e != cudaSuccess) return (int)e;
     void* args[] = {&P};
-    e = cudaLaunchKernel(fn, dim3(plan.ctas), dim3(plan.threads), args, plan.smem_bytes,
-                         (cudaStream_t)stream);
+    e = cudaLaunchKernel(fn, dim3(plan.ctas), dim3(plan.threads), args, plan.smem_bytes, (cudaStream_t)stream);
     return (int)e;
 }
 
