@@ -181,6 +181,13 @@ struct ImageBuilder {
     uint16_t* u16(uint32_t off) { return reinterpret_cast<uint16_t*>(buf.data() + off); }
 };
 
+inline uint32_t reverse_bits(uint32_t x)
+{
+    uint32_t r = 0;
+    for (int b = 0; b < 32; ++b) r |= ((x >> b) & 1u) << (31 - b);
+    return r;
+}
+
 // Table entry idx of function f (parents[0] is the MSB of idx, reading Q5).
 inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
 {
@@ -224,25 +231,23 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
         }
         uint32_t w3 = 0;  // nrec[i].w, written last (B.alloc may move the buffer)
         if (fast[i]) {
-            const uint32_t off_desc = B.alloc(16u * ell);
+            const int32_t tm = FT;  // every fast function is padded to the model-wide FT
+            const uint32_t off_desc = B.alloc((size_t)pbn::kDescBytes * ell, 8);
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;
                 const int32_t theta = d->par_off[f + 1] - d->par_off[f];
-                // table padded to FT index bits: dummy parents are the low bits
+                // table padded to theta_max index bits: dummy parents are the low bits
                 uint64_t T = 0;
-                for (uint32_t idx = 0; idx < (1u << FT); ++idx)
-                    T |= (uint64_t)table_bit(d, f, idx >> (FT - theta)) << idx;
+                for (uint32_t idx = 0; idx < (1u << tm); ++idx)
+                    T |= (uint64_t)table_bit(d, f, idx >> (tm - theta)) << idx;
+                const uint32_t off = off_desc + pbn::kDescBytes * (uint32_t)j;
+                // stored bit-reversed per word: entry e at bit 31 - (e & 31)
+                B.u32(off)[0] = reverse_bits((uint32_t)T);
+                B.u32(off)[1] = reverse_bits((uint32_t)(T >> 32));
                 // padded parent list, MSB first; dummies read node 0
-                const uint32_t off_par = B.alloc(2u * (size_t)FT, 4);
-                uint16_t* par = B.u16(off_par);
-                for (int32_t m = 0; m < FT; ++m)
+                uint16_t* par = B.u16(off + 8u);
+                for (int32_t m = 0; m < tm; ++m)
                     par[m] = (uint16_t)(m < theta ? 4u * d->parents[d->par_off[f] + m] : 0u);
-                uint32_t* desc = B.u32(off_desc + 16u * j);
-                desc[0] = (uint32_t)T;
-                desc[1] = (uint32_t)(T >> 32);
-                desc[2] = off_par;
-                desc[3] = 0;
-                reloc.push_back(off_desc + 16u * j + 8u);
             }
             w3 = off_desc;
         } else {
@@ -274,7 +279,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
             sr[3] = 0;
             reloc.push_back(off_slow);
             reloc.push_back(off_slow + 8u);
-            w3 = off_slow | pbn::kSlowFlag;
+            w3 = off_slow | pbn::kSlowNode;
         }
         uint32_t* rec = B.u32(off_nrec + 16u * i);
         for (int k = 0; k < 3; ++k) rec[k] = k < (int)E.size() ? E[k] : 0xFFFFFFFFu;

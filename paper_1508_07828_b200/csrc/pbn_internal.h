@@ -10,18 +10,21 @@
 //       E_k  selection thresholds of reading Q3 as E_k = D_k - 1: the
 //            selected function is j = #{k : u > E_k}; unused = 0xFFFFFFFF
 //       w    FAST node (ell <= 4, theta_max <= 6): offset of the node's first
-//            fast descriptor (16-aligned, low bits 0)
-//            SLOW node (anything else): offset of its slow record | 1
-//   fast descriptor (uint4, per function of a fast node)   {t0, t1, plist, 0}
+//            fast descriptor (8-aligned, low 3 bits 0)
+//            SLOW node (anything else): offset of its slow record | 7
+//   fast descriptor (24 bytes, per function of a fast node, consecutive)
+//            {t0, t1, par[0..FT-1] (u16)}
 //       every fast function is PADDED to the model-wide fast width FT (the
 //       largest theta over fast nodes, 3 <= FT <= 6): its parent list is
 //       extended with dummy parents that the table ignores
 //       (table'[idx'] = table[idx' >> (FT - theta)]), so every lane of a warp
-//       gathers exactly FT parents whatever function it chose -- the gather is
-//       straight-line code with a compile-time trip count.
-//       t0,t1  the padded 2^FT-entry table (entries 0-31 in t0, 32-63 in t1)
-//       plist  offset of the padded parent list: FT u16 entries holding
-//              (parent node * 4), MSB first (parents[0] first, reading Q5)
+//       gathers exactly FT parents whatever function it chose -- straight-line
+//       code with a compile-time trip count.
+//       t0,t1  the padded 2^FT-entry table, entries 0-31 in t0 and 32-63 in t1,
+//              each word BIT-REVERSED (entry e at bit 31 - (e & 31)) so the
+//              kernel reads an entry as the sign bit of (word << (e & 31))
+//       par    (parent node * 4) for m < FT, MSB first (parents[0] first,
+//              reading Q5); the pad entries read node 0
 //   slow record (uint4, per slow node)  {thr, ell, gdesc, 0}
 //       thr    offset of ell-1 u32 thresholds E_1..E_{ell-1}
 //       gdesc  offset of ell generic descriptors
@@ -29,8 +32,8 @@
 //       toff   offset of the ceil(2^theta/32) table words; poff: u16 parent list
 //              (node*4), parents[0] first (MSB, reading Q5)
 //   relocation list (u32, stored after the image in device memory, not staged)
-//       byte offsets of every offset-valued word above (nrec.w, plist, thr,
-//       gdesc, toff, poff).  After staging, each CTA adds its shared-memory
+//       byte offsets of every offset-valued word above (nrec.w, thr, gdesc,
+//       toff, poff).  After staging, each CTA adds its shared-memory
 //       base to those words, so the hot loop uses absolute shared addresses.
 //
 // The thresholds are the product's own computation of reading Q3
@@ -42,7 +45,8 @@ namespace pbn {
 
 constexpr int kMaxPred = 16;
 constexpr int kMaxWarpsPerCta = 32;
-constexpr uint32_t kSlowFlag = 1;
+constexpr uint32_t kSlowNode = 7;   // nrec.w low bits marking a slow node
+constexpr uint32_t kDescBytes = 24;  // fast descriptor stride
 constexpr int kFastMaxTheta = 6;
 constexpr int kFastMinTheta = 3;
 constexpr int kFastMaxEll = 4;

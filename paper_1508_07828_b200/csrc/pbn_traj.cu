@@ -75,6 +75,59 @@ __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
     return make_uint4(c0, c1, c2, c3);
 }
 
+// The same generator split for the step loop.  With counter (q, chain, t_lo,
+// t_hi), the parts of rounds 1-2 that depend only on (chain, t) are computed
+// once per step (PhiloxStep); philox_quad finishes the 10 rounds for quad q.
+struct PhiloxStep {
+    uint32_t c0r1;   // round-1 output word 0: hi(M1 t_lo) ^ chain ^ k0
+    uint32_t c1r1;   // round-1 output word 1: lo(M1 t_lo)
+    uint32_t hi0r2;  // round-2 hi(M0 c0r1)
+    uint32_t lo0r2;  // round-2 lo(M0 c0r1) = round-2 output word 3
+    uint32_t t_hi;
+};
+
+__device__ __forceinline__ PhiloxStep philox_step(uint32_t chain, uint32_t t_lo, uint32_t t_hi,
+                                                  const uint32_t* __restrict__ rk)
+{
+    PhiloxStep s;
+    uint32_t lo1, hi1;
+    mulhilo(t_lo, 0xCD9E8D57u, lo1, hi1);
+    s.c0r1 = hi1 ^ chain ^ rk[0];
+    s.c1r1 = lo1;
+    mulhilo(s.c0r1, 0xD2511F53u, s.lo0r2, s.hi0r2);
+    s.t_hi = t_hi;
+    return s;
+}
+
+__device__ __forceinline__ uint4 philox_quad(uint32_t q, const PhiloxStep& s, const uint32_t* __restrict__ rk)
+{
+    // round 1 (quad part): (hi0, lo0) = M0 q
+    uint32_t lo0, hi0;
+    mulhilo(q, 0xD2511F53u, lo0, hi0);
+    const uint32_t c2r1 = hi0 ^ s.t_hi ^ rk[1];
+    const uint32_t c3r1 = lo0;
+    // round 2: M0 * c0r1 is per step; M1 * c2r1 per quad
+    uint32_t lo1, hi1;
+    mulhilo(c2r1, 0xCD9E8D57u, lo1, hi1);
+    uint32_t c0 = hi1 ^ s.c1r1 ^ rk[2];
+    uint32_t c1 = lo1;
+    uint32_t c2 = s.hi0r2 ^ c3r1 ^ rk[3];
+    uint32_t c3 = s.lo0r2;
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        uint32_t a0, b0, a1, b1;
+        mulhilo(c0, 0xD2511F53u, a0, b0);
+        mulhilo(c2, 0xCD9E8D57u, a1, b1);
+        const uint32_t n0 = b1 ^ c1 ^ rk[2 * r];
+        const uint32_t n2 = b0 ^ c3 ^ rk[2 * r + 1];
+        c1 = a1;
+        c3 = a0;
+        c0 = n0;
+        c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
 {
@@ -102,6 +155,12 @@ __device__ __forceinline__ uint32_t lds16_ro(uint32_t a)
     asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return (uint32_t)v;
 }
+__device__ __forceinline__ uint2 lds64_ro(uint32_t a)
+{
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint4 lds128_ro(uint32_t a)
 {
     uint4 v;
@@ -111,6 +170,33 @@ __device__ __forceinline__ uint4 lds128_ro(uint32_t a)
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v)
 {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// State words of the current buffer.  Not volatile, so loads of different
+// nodes interleave freely; they are ordered after each step barrier by
+// making the buffer base opaque there (fence_state below).
+__device__ __forceinline__ uint32_t lds32_state(uint32_t a)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void fence_state(uint32_t& a, uint32_t& b)
+{
+    asm volatile("" : "+r"(a), "+r"(b)::"memory");
+}
+// 16-byte store of four consecutive words by one lane when pred != 0
+__device__ __forceinline__ void sts128_if(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t pred)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(a),
+        "r"(x), "r"(y), "r"(z), "r"(w), "r"(pred)
+        : "memory");
+}
+__device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, uint32_t pred)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
+                 "r"(pred)
+                 : "memory");
 }
 
 
@@ -124,6 +210,11 @@ struct Img {
     {
         if (SMEM) return lds128_ro(a);
         return __ldg(reinterpret_cast<const uint4*>(gbase + a));
+    }
+    __device__ __forceinline__ uint2 ld64(uint32_t a) const
+    {
+        if (SMEM) return lds64_ro(a);
+        return __ldg(reinterpret_cast<const uint2*>(gbase + a));
     }
     __device__ __forceinline__ uint32_t ld32(uint32_t a) const
     {
@@ -157,45 +248,84 @@ __device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w,
 }
 
 // One node of one step for the warp's 32 chains (A4-A7).  Returns the gamma word.
+// Split a u32 holding two u16 parent offsets (low half = first) on the FMA
+// pipe: hi = x >> 16 as a mul-high, lo = x - hi * 2^16 as a mul-add.
+__device__ __forceinline__ void split_pair(uint32_t x, uint32_t& lo, uint32_t& hi)
+{
+    asm("mul.hi.u32 %1, %2, 65536;\n\tmad.lo.u32 %0, %1, 0xFFFF0000, %2;" : "=r"(lo), "=r"(hi) : "r"(x));
+}
+
+// idx += B when this lane's bit of the parent word is set: one LOP3 producing a
+// predicate (ALU pipe) and one predicated add (FMA pipe).
+template <uint32_t B>
+__device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t lmask)
+{
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+        "@p add.u32 %0, %0, %3;\n\t}"
+        : "+r"(idx)
+        : "r"(wv), "r"(lmask), "n"(B));
+}
+
+// One node of one step for the warp's 32 chains (A4-A7): returns the node's
+// new state word (bit l = chain of lane l) and its gamma word in *gw_out.
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
-__device__ __forceinline__ uint32_t step_node(const Img<SMEM>& img, uint32_t rec_addr, uint32_t i, uint32_t u,
-                                              uint32_t Tp, uint32_t old, uint32_t nw, uint32_t gam, uint32_t rot,
-                                              bool leader)
+__device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec_addr, uint32_t i, uint32_t u,
+                                              uint32_t Tp, uint32_t old, uint32_t lmask, uint32_t rot,
+                                              uint32_t& gw_out)
 {
     const uint4 rec = img.ld128(rec_addr);
     const uint32_t gw = __ballot_sync(FULL, u < Tp);  // gamma_i(t) = 1 (A4)
     uint32_t bit;
-    if (!SLOW || !(rec.w & kSlowFlag)) {
+    if (!SLOW || (rec.w & 7u) != kSlowNode) {
         // A5: descriptor of function j = #{k : u > E_k}
         uint32_t dp = rec.w;
-        if (u > rec.x) dp += 16u;
-        if (u > rec.y) dp += 16u;
-        if (u > rec.z) dp += 16u;
-        const uint4 d = img.ld128(dp);  // {t0, t1, plist, 0}
-        // A6: gather the FT padded parents, MSB first: rotate bit `lane` of the
-        // parent word to bit 31, funnel it into the index
-        uint32_t idx = 0;
-#pragma unroll
-        for (int k = 0; k < FT; ++k) {
-            const uint32_t off = img.ld16(d.z + 2u * k);
-            const uint32_t wv = lds32(old + off);
-            idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+        if (u > rec.x) dp += kDescBytes;
+        if (u > rec.y) dp += kDescBytes;
+        if (u > rec.z) dp += kDescBytes;
+        const uint2 t = img.ld64(dp);  // padded table (bit-reversed words)
+        // FT padded parent offsets, MSB first, two per u32
+        uint32_t off[6];
+        {
+            uint32_t w01, w23 = 0, w45 = 0;
+            if (FT > 2) {
+                const uint2 a = img.ld64(dp + 8u);
+                w01 = a.x;
+                w23 = a.y;
+            } else {
+                w01 = img.ld32(dp + 8u);
+            }
+            if (FT > 4) w45 = img.ld32(dp + 16u);
+            split_pair(w01, off[0], off[1]);
+            split_pair(w23, off[2], off[3]);
+            split_pair(w45, off[4], off[5]);
         }
-        const uint32_t tw = (FT == 6 && idx >= 32u) ? d.y : d.x;
-        bit = (tw >> (idx & 31u)) & 1u;
+        // A6: gather: parent k contributes bit (FT-1-k) of the table index when
+        // bit `lane` of its state word is set (LOP3 -> predicate, predicated add)
+        // FT = 6: the first (most significant) parent picks the table word
+        // (entries 32-63 in t1), the other five index within it
+        uint32_t tw = t.x;
+        if (FT == 6) tw = (lds32_state(old + off[0]) & lmask) ? t.y : t.x;
+        constexpr int S = FT == 6 ? 1 : 0;  // first parent handled above
+        constexpr int R = FT - S;          // parents indexing within the word
+        uint32_t idx = 0;
+        if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(old + off[S + 0]), lmask);
+        if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(old + off[S + 1]), lmask);
+        if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(old + off[(S + 2) % 6]), lmask);
+        if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(old + off[(S + 3) % 6]), lmask);
+        if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(old + off[(S + 4) % 6]), lmask);
+        // the table words are stored bit-REVERSED (entry e at bit 31 - (e & 31)),
+        // so the entry is the sign bit of the word shifted left by idx
+        bit = (uint32_t)((int32_t)(tw << idx) < 0);
     } else {
         bit = slow_node_bit<SMEM>(img, rec.w, u, old, rot);
     }
     uint32_t nb = __ballot_sync(FULL, bit != 0u);  // commit (A7)
     if (PER_NODE) {
-        const uint32_t ow = lds32(old + 4u * i);
+        const uint32_t ow = lds32_state(old + 4u * i);
         nb = (nb & ~gw) | (~ow & gw);
     }
-    if (leader) {
-        sts32(nw + 4u * i, nb);
-        if (!PER_NODE) sts32(gam + 4u * i, gw);
-    }
-    return gw;
+    gw_out = gw;
+    return nb;
 }
 
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
@@ -251,7 +381,9 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
     const bool valid = chain_local < P.n_chains;
     const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
     const bool leader = lane == 0;
-    const uint32_t rot = 31u - (uint32_t)lane;  // rotate-left amount: bit `lane` -> bit 31
+    const uint32_t lead = leader ? FULL : 0u;        // store predicate as a word
+    const uint32_t rot = 31u - (uint32_t)lane;       // rotate-left amount: bit `lane` -> bit 31
+    const uint32_t lmask = 1u << lane;               // this chain's bit in a state word
 
     const uint32_t gbase = sbase + P.image_smem_bytes;
     uint32_t bufA = gbase;                       // current state s_{t-1}
@@ -290,6 +422,8 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             }
         }
     }
+    if (!PER_NODE)
+        for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
     __syncthreads();
 
     // ---- per-lane statistics (warp 0) ----
@@ -303,40 +437,70 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         const uint64_t t = (uint64_t)(P.step0 + r);
         const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
         uint32_t any = 0;
-        for (int q = q0; q < q1; ++q) {
-            const uint4 rw = philox4x32_10((uint32_t)q, chain, t_lo, t_hi, P.rk);
+        const PhiloxStep ps = philox_step(chain, t_lo, t_hi, P.rk);
+        const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
+        // software pipeline: the next quad's Philox words are computed while
+        // this quad's nodes gather (independent instruction streams)
+        uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
+        for (int q = q0; q < qf; ++q) {
+            const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
             const uint32_t i0 = 4u * (uint32_t)q;
             const uint32_t ra = nrec + 16u * i0;
-            if (full_quads || q + 1 < P.nquads) {
-                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra, i0, rw.x, Tp, bufA, bufB, gam, rot, leader);
-                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u, i0 + 1, rw.y, Tp, bufA, bufB, gam, rot,
-                                                           leader);
-                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 32u, i0 + 2, rw.z, Tp, bufA, bufB, gam, rot,
-                                                           leader);
-                any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 48u, i0 + 3, rw.w, Tp, bufA, bufB, gam, rot,
-                                                           leader);
-            } else {
+            // the quad's four nodes are independent: compute all, then one
+            // 16-byte store commits them (and their gamma words if any)
+            uint32_t g0, g1, g2, g3;
+            const uint32_t w0 = node_word<SMEM, PER_NODE, FT, SLOW>(img, ra, i0, rw.x, Tp, bufA, lmask, rot, g0);
+            const uint32_t w1 =
+                node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u, i0 + 1, rw.y, Tp, bufA, lmask, rot, g1);
+            const uint32_t w2 =
+                node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 32u, i0 + 2, rw.z, Tp, bufA, lmask, rot, g2);
+            const uint32_t w3 =
+                node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 48u, i0 + 3, rw.w, Tp, bufA, lmask, rot, g3);
+            sts128_if(bufB + 4u * i0, w0, w1, w2, w3, lead);
+            if (!PER_NODE) {
+                const uint32_t g = g0 | g1 | g2 | g3;
+                any |= g;
+                // gamma words only when nonzero (rare); the fixup clears them
+                sts128_if(gam + 4u * i0, g0, g1, g2, g3, g & lead);
+            }
+            rw = rn;
+        }
+        if (qf < q1) {  // ragged last quad (n % 4 != 0), node by node
+            {
+                const int q = qf;
+                const uint32_t i0 = 4u * (uint32_t)q;
+                const uint32_t ra = nrec + 16u * i0;
                 const uint32_t rr[4] = {rw.x, rw.y, rw.z, rw.w};
-                for (uint32_t k = 0; k < 4 && (int)(i0 + k) < n; ++k)
-                    any |= step_node<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u * k, i0 + k, rr[k], Tp, bufA, bufB, gam,
-                                                               rot, leader);
+                for (uint32_t k = 0; k < 4 && (int)(i0 + k) < n; ++k) {
+                    uint32_t gk;
+                    const uint32_t wk = node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u * k, i0 + k, rr[k], Tp,
+                                                                            bufA, lmask, rot, gk);
+                    sts32_if(bufB + 4u * (i0 + k), wk, lead);
+                    if (!PER_NODE) {
+                        any |= gk;
+                        sts32_if(gam + 4u * (i0 + k), gk, gk & lead);
+                    }
+                }
             }
         }
         if (!PER_NODE && leader) sts32(anyw + 4u * wg, any);
         __syncthreads();
+        fence_state(bufA, bufB);
         if (!PER_NODE) {
             // VECTOR: chains with any gamma take s XOR gamma instead of f(s)
-            uint32_t M = 0;
-            for (int w = 0; w < W; ++w) M |= lds32(anyw + 4u * w);
+            const uint32_t M = __reduce_or_sync(FULL, lane < W ? lds32(anyw + 4u * lane) : 0u);
             if (M) {
                 const int lo = 4 * q0, hi = min(4 * q1, n);
                 for (int i = lo + lane; i < hi; i += 32) {
                     const uint32_t a = 4u * (uint32_t)i;
-                    const uint32_t f = lds32(bufB + a), o = lds32(bufA + a), gmm = lds32(gam + a);
+                    const uint32_t gmm = lds32(gam + a);
+                    if (gmm) sts32(gam + a, 0u);  // keep the gamma buffer all-zero
+                    const uint32_t f = lds32(bufB + a), o = lds32(bufA + a);
                     sts32(bufB + a, (f & ~M) | ((o ^ gmm) & M));
                 }
             }
             __syncthreads();
+            fence_state(bufA, bufB);
         }
         if (wg == 0 && r > P.burn_in) {
             // A8: property indicator, bit-sliced over the group's chains
