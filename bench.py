@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=2500)
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--schedule", type=int, default=0, help="0 auto, 1 CTA per group, 2 persistent")
+    ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
@@ -223,6 +225,7 @@ def main():
         pbn.pbn_simulate(pm, out, n_chains=chains, chain_base=chain_base, steps=window,
                          burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=True,
                          emit_bits=True, groups_per_cta=args.groups, warps_per_group=args.warps,
+                         schedule=args.schedule, chunk_steps=args.chunk,
                          stream=stream)
 
     for _ in range(args.warmup):

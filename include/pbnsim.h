@@ -136,8 +136,13 @@ typedef struct {
  *                bits_offset are kept, bits above must be 0), every other
  *                touched word is overwritten
  *   bits_row_words  row stride of `bits` in u32 (0 = ceil(steps/32))
- *   groups_per_cta, warps_per_group: launch-shape overrides (0 = auto);
- *                results never depend on them. */
+ *   groups_per_cta  0 or 1 (one 32-chain group per CTA in this build)
+ *   warps_per_group warps sharing one group's nodes (0 = auto, <= 32)
+ *   schedule     0 auto; 1 one CTA per group; 2 persistent CTAs pulling
+ *                (group, chunk of chunk_steps steps) units, state carried
+ *                between chunks in a stream-ordered scratch allocation
+ *   chunk_steps  persistent chunk length (0 = auto)
+ * The launch-shape fields never change any output. */
 typedef struct {
     int64_t n_chains;
     int64_t chain_base;
@@ -153,6 +158,8 @@ typedef struct {
     int64_t bits_row_words;
     int32_t groups_per_cta;
     int32_t warps_per_group;
+    int32_t schedule;
+    int64_t chunk_steps;
 } pbn_sim_args;
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).

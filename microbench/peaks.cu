@@ -43,9 +43,10 @@ __global__ void __launch_bounds__(1024, 2) kbench(uint32_t seed)
     __syncthreads();
     const unsigned long long t0 = clock64();
 #pragma unroll 1
-    for (int it = 0; it < ITERS; ++it) {
+    for (int it = 0; it < ITERS; it += 8) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int kk = 0; kk < 64; ++kk) {
+            const int k = kk & 7;
             if (OP == 0) {  // LOP3 (3-input XOR)
                 asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[k]) : "r"(s[k]), "r"(lmask));
             } else if (OP == 1) {  // IADD (add.u32 -> IADD3 / VIADD)

@@ -60,7 +60,8 @@ class pbn_sim_args(C.Structure):
                 ("burn_in", C.c_int64), ("steps", C.c_int64), ("batch", C.c_int64),
                 ("seed", C.c_uint64), ("pred", pbn_predicate), ("init", C.c_int32),
                 ("emit_bits", C.c_int32), ("bits_offset", C.c_int64), ("bits_row_words", C.c_int64),
-                ("groups_per_cta", C.c_int32), ("warps_per_group", C.c_int32)]
+                ("groups_per_cta", C.c_int32), ("warps_per_group", C.c_int32),
+                ("schedule", C.c_int32), ("chunk_steps", C.c_int64)]
 
 
 class pbn_sim_out(C.Structure):

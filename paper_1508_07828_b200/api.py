@@ -151,13 +151,13 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                  step0: int = 0, burn_in: int = 0, batch: int = 0, seed: int = 0, pred=None,
                  init: bool = False, emit_bits: bool = False, bits_offset: int = 0,
                  bits_row_words: int = 0, groups_per_cta: int = 0, warps_per_group: int = 0,
-                 stream=None) -> None:
+                 schedule: int = 0, chunk_steps: int = 0, stream=None) -> None:
     cp, _keep = _pred(pred)
     a = L.pbn_sim_args(n_chains=n_chains, chain_base=chain_base, step0=step0, burn_in=burn_in,
                        steps=steps, batch=batch, seed=seed, pred=cp, init=int(bool(init)),
                        emit_bits=int(bool(emit_bits)), bits_offset=bits_offset,
                        bits_row_words=bits_row_words, groups_per_cta=groups_per_cta,
-                       warps_per_group=warps_per_group)
+                       warps_per_group=warps_per_group, schedule=schedule, chunk_steps=chunk_steps)
     o = out.c_struct()
     check(lib().pbn_simulate(model.handle, C.byref(a), C.byref(o), _stream_handle(stream)))
 

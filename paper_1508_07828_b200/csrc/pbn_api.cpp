@@ -456,7 +456,8 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     int rc = pbn::plan_traj_launch(P, m->device, a->warps_per_group, &plan, &why);
     if (rc < 0) return PBN_E_USAGE;
     if (rc > 0) return PBN_E_CUDA;
-    rc = pbn::launch_traj(P, plan, stream);
+    if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0) return PBN_E_USAGE;
+    rc = pbn::launch_traj(P, plan, m->device, a->schedule, a->chunk_steps, stream);
     return rc == 0 ? PBN_OK : PBN_E_CUDA;
 }
 

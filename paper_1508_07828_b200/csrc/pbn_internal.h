@@ -79,6 +79,15 @@ struct TrajParams {
     int32_t pred_k;
     uint16_t pred_node[kMaxPred];
     uint8_t pred_val[kMaxPred];
+    // persistent scheduling (grid = resident CTAs; units = (group, step chunk))
+    int32_t persistent;
+    int64_t n_groups;          // ceil(n_chains / 32)
+    int64_t chunk_steps;       // steps per unit
+    int64_t total_units;       // n_groups * ceil(total steps / chunk_steps)
+    unsigned long long* work_ctr;  // unit queue head (zeroed per launch)
+    uint32_t* done;            // [n_groups] chunks completed per group (zeroed per launch)
+    uint32_t* scratch;         // [n_groups x scratch_stride] suspended group state
+    int64_t scratch_stride;    // n_pad + 8 * 32 words
     int64_t batch_row;         // ceil(steps/batch) (0 if no batches)
     int64_t bits_row;          // row stride of bits in u32
     int64_t bits_offset;       // window element w -> row bit bits_offset + w
@@ -104,7 +113,8 @@ struct LaunchPlan {
 // Implemented in pbn_traj.cu.  Returns 0 on success, a cudaError_t value on a
 // CUDA failure, or -1 (with *why set) when the sizes cannot be served.
 int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why);
-int launch_traj(TrajParams P, const LaunchPlan& plan, void* stream);
+// schedule: 0 auto, 1 one CTA per 32-chain group, 2 persistent (chunk_steps 0 = auto)
+int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* stream);
 
 struct RecountParams {
     const uint32_t* bits;

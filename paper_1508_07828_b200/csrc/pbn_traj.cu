@@ -171,19 +171,16 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v)
 {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-// State words of the current buffer.  Not volatile, so loads of different
-// nodes interleave freely; they are ordered after each step barrier by
-// making the buffer base opaque there (fence_state below).
+// State words of the current buffer.  `asm volatile` keeps them on the right
+// side of the step barriers at the compiler level; the plain ld.shared lets
+// ptxas interleave the loads of different nodes freely.
 __device__ __forceinline__ uint32_t lds32_state(uint32_t a)
 {
     uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
-__device__ __forceinline__ void fence_state(uint32_t& a, uint32_t& b)
-{
-    asm volatile("" : "+r"(a), "+r"(b)::"memory");
-}
+__device__ __forceinline__ void fence_state(uint32_t&, uint32_t&) {}
 // 16-byte store of four consecutive words by one lane when pred != 0
 __device__ __forceinline__ void sts128_if(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t pred)
 {
@@ -377,63 +374,121 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         __syncthreads();
     }
 
-    const int64_t chain_local = (int64_t)blockIdx.x * 32 + lane;
-    const bool valid = chain_local < P.n_chains;
-    const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
     const bool leader = lane == 0;
     const uint32_t lead = leader ? FULL : 0u;        // store predicate as a word
     const uint32_t rot = 31u - (uint32_t)lane;       // rotate-left amount: bit `lane` -> bit 31
     const uint32_t lmask = 1u << lane;               // this chain's bit in a state word
 
     const uint32_t gbase = sbase + P.image_smem_bytes;
-    uint32_t bufA = gbase;                       // current state s_{t-1}
-    uint32_t bufB = gbase + 4u * P.n_pad;        // next state s_t
     const uint32_t gam = gbase + 8u * P.n_pad;   // VECTOR: gamma words
     const uint32_t anyw = gbase + 4u * (PER_NODE ? 2 : 3) * P.n_pad;  // [W]
     const uint32_t nrec = SMEM ? sbase : 0u;     // node records start the image
 
     const int q0 = (int)((int64_t)wg * P.nquads / W);
     const int q1 = (int)((int64_t)(wg + 1) * P.nquads / W);
+    const int nsw = P.state_words;
+    const int b0 = (int)((int64_t)wg * nsw / W), b1 = (int)((int64_t)(wg + 1) * nsw / W);
 
-    // ---- A2: initial state ----
-    if (P.init) {
-        for (int q = q0; q < q1; ++q) {
-            const uint4 r = philox4x32_10((uint32_t)q, chain, 0u, 0u, P.rk);
-            const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+    if (!PER_NODE)  // the gamma buffer is all-zero between steps (the fixup clears it)
+        for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
+
+    const int64_t total = P.burn_in + P.steps;
+    const uint32_t Tp = P.Tp;
+    const bool full_quads = (n & 3) == 0 || q1 < P.nquads;  // this warp never sees a ragged quad
+    __shared__ unsigned long long s_unit;
+
+    // ---- work units: (group, chunk of steps).  Non-persistent launches run one
+    // unit per CTA (its group, all steps); persistent launches pull units from a
+    // queue, chunk c of group g after chunk c-1 (flag done[g]), and carry the
+    // group's bit-sliced state and per-lane counters across chunks in scratch.
+    for (int64_t it = 0;; ++it) {
+        int64_t group, chunk, r_begin, r_end;
+        if (!P.persistent) {
+            if (it > 0) break;
+            group = blockIdx.x;
+            chunk = 0;
+            r_begin = 1;
+            r_end = total;
+        } else {
+            __syncthreads();  // s_unit free for reuse
+            if (tid == 0) s_unit = atomicAdd(P.work_ctr, 1ull);
+            __syncthreads();
+            // redux makes the unit index a uniform value (UR), so the loop stays
+            // warp-uniform and the buffer bases stay in uniform registers
+            const unsigned long long u = __reduce_max_sync(FULL, (uint32_t)s_unit);
+            if (u >= (unsigned long long)P.total_units) break;
+            group = (int64_t)(u % (unsigned long long)P.n_groups);
+            chunk = (int64_t)(u / (unsigned long long)P.n_groups);
+            r_begin = chunk * P.chunk_steps + 1;
+            r_end = min(total, (chunk + 1) * P.chunk_steps);
+            if (chunk > 0 && tid == 0) {
+                // wait for chunk c-1 of this group (acquire)
+                for (;;) {
+                    unsigned int d;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(P.done + group) : "memory");
+                    if ((int64_t)d >= chunk) break;
+                    __nanosleep(256);
+                }
+            }
+        }
+        const bool first_chunk = chunk == 0;
+        const bool last_chunk = r_end >= total;
+        const int64_t chain_local = group * 32 + lane;
+        const bool valid = chain_local < P.n_chains;
+        const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
+        uint32_t bufA = gbase;                  // current state s_{t-1}
+        uint32_t bufB = gbase + 4u * P.n_pad;   // next state s_t
+        uint32_t* scr = P.scratch + group * (int64_t)P.scratch_stride;  // persistent only
+
+        // ---- per-lane statistics (warp 0) ----
+        uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0, bcount = 0;
+
+        if (!first_chunk) {
+            // resume: bit-sliced state words and warp-0 counters from scratch
+            __syncthreads();
+            for (int i = tid; i < n; i += blockDim.x) sts32(bufA + 4u * i, __ldcg(scr + i));
+            if (wg == 0) {
+                const uint32_t* st = scr + P.n_pad + 8 * lane;
+                c1 = __ldcg(st + 0);
+                n01 = __ldcg(st + 1);
+                n10 = __ldcg(st + 2);
+                first = __ldcg(st + 3);
+                prev = __ldcg(st + 4);
+                bacc = __ldcg(st + 5);
+                bitw = __ldcg(st + 6);
+                bcount = __ldcg(st + 7);
+            }
+        } else if (P.init) {
+            // ---- A2: initial state s_0[i] = u(chain, 0, i) >> 31 ----
+            for (int q = q0; q < q1; ++q) {
+                const uint4 r = philox4x32_10((uint32_t)q, chain, 0u, 0u, P.rk);
+                const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = 4 * q + k;
-                if (i < n) {
-                    const uint32_t wv = __ballot_sync(FULL, (rr[k] >> 31) != 0u);
+                for (int k = 0; k < 4; ++k) {
+                    const int i = 4 * q + k;
+                    if (i < n) {
+                        const uint32_t wv = __ballot_sync(FULL, (rr[k] >> 31) != 0u);
+                        if (leader) sts32(bufA + 4u * i, wv);
+                    }
+                }
+            }
+        } else {
+            for (int b = b0; b < b1; ++b) {
+                const uint32_t v = valid ? P.state[chain_local * nsw + b] : 0u;
+                for (int k = 0; k < 32; ++k) {
+                    const int i = 32 * b + k;
+                    if (i >= n) break;
+                    const uint32_t wv = __ballot_sync(FULL, (v >> k) & 1u);
                     if (leader) sts32(bufA + 4u * i, wv);
                 }
             }
         }
-    } else {
-        const int nb = P.state_words;
-        const int b0 = (int)((int64_t)wg * nb / W), b1 = (int)((int64_t)(wg + 1) * nb / W);
-        for (int b = b0; b < b1; ++b) {
-            const uint32_t v = valid ? P.state[chain_local * nb + b] : 0u;
-            for (int k = 0; k < 32; ++k) {
-                const int i = 32 * b + k;
-                if (i >= n) break;
-                const uint32_t wv = __ballot_sync(FULL, (v >> k) & 1u);
-                if (leader) sts32(bufA + 4u * i, wv);
-            }
-        }
-    }
-    if (!PER_NODE)
-        for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
-    __syncthreads();
+        __syncthreads();
 
-    // ---- per-lane statistics (warp 0) ----
-    uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0;
-    int64_t bcount = 0;  // elements in the current batch
-    const int64_t total = P.burn_in + P.steps;
-    const uint32_t Tp = P.Tp;
-    const bool full_quads = (n & 3) == 0 || q1 < P.nquads;  // this warp never sees a ragged quad
-
-    for (int64_t r = 1; r <= total; ++r) {
+    // one synchronous step s_{t-1} (bufA) -> s_t (bufB); the step loop below is
+    // unrolled by two with the buffer roles fixed in each half, so the buffer
+    // bases stay loop-invariant (uniform registers, [R+UR] addressing)
+    auto step = [&](const int64_t r, const uint32_t bufA, const uint32_t bufB) {
         const uint64_t t = (uint64_t)(P.step0 + r);
         const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
         uint32_t any = 0;
@@ -485,7 +540,6 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         }
         if (!PER_NODE && leader) sts32(anyw + 4u * wg, any);
         __syncthreads();
-        fence_state(bufA, bufB);
         if (!PER_NODE) {
             // VECTOR: chains with any gamma take s XOR gamma instead of f(s)
             const uint32_t M = __reduce_or_sync(FULL, lane < W ? lds32(anyw + 4u * lane) : 0u);
@@ -500,8 +554,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                 }
             }
             __syncthreads();
-            fence_state(bufA, bufB);
-        }
+            }
         if (wg == 0 && r > P.burn_in) {
             // A8: property indicator, bit-sliced over the group's chains
             uint32_t Iw = FULL;
@@ -545,15 +598,43 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                 }
             }
         }
-        const uint32_t tmp = bufA;  // bufA now holds the newest state
+    };
+    for (int64_t r = r_begin; r <= r_end; r += 2) {
+        step(r, bufA, bufB);
+        if (r + 1 <= r_end) step(r + 1, bufB, bufA);
+    }
+    if (r_end >= r_begin && ((r_end - r_begin + 1) & 1)) {  // bufA holds the newest state
+        const uint32_t tmp = bufA;
         bufA = bufB;
         bufB = tmp;
     }
 
+    if (!last_chunk) {
+        // suspend: bit-sliced state and warp-0 counters to scratch, then
+        // release chunk c+1 of this group
+        for (int i = tid; i < n; i += blockDim.x) __stcg(scr + i, lds32(bufA + 4u * i));
+        if (wg == 0) {
+            uint32_t* st = scr + P.n_pad + 8 * lane;
+            __stcg(st + 0, c1);
+            __stcg(st + 1, n01);
+            __stcg(st + 2, n10);
+            __stcg(st + 3, first);
+            __stcg(st + 4, prev);
+            __stcg(st + 5, bacc);
+            __stcg(st + 6, bitw);
+            __stcg(st + 7, bcount);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.done + group), "r"((uint32_t)(chunk + 1))
+                         : "memory");
+        }
+        continue;
+    }
+
     // ---- epilogue: final state back to chain-major rows ----
     {
-        const int nb = P.state_words;
-        const int b0 = (int)((int64_t)wg * nb / W), b1 = (int)((int64_t)(wg + 1) * nb / W);
         for (int b = b0; b < b1; ++b) {
             uint32_t v = 0;
             for (int k = 0; k < 32; ++k) {
@@ -561,7 +642,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                 if (i >= n) break;
                 v |= ((lds32(bufA + 4u * i) >> lane) & 1u) << k;
             }
-            if (valid) P.state[chain_local * nb + b] = v;
+            if (valid) P.state[chain_local * nsw + b] = v;
         }
     }
     if (wg == 0) {
@@ -598,6 +679,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             }
         }
     }
+    }  // work units
 }
 
 // kernel table: [SMEM][PER_NODE][FT-3][SLOW]
@@ -616,6 +698,13 @@ const void* pick_ft(int FT, bool slow)
         case 5: return slow ? kptr<SMEM, PER_NODE, 5, true>() : kptr<SMEM, PER_NODE, 5, false>();
         default: return slow ? kptr<SMEM, PER_NODE, 6, true>() : kptr<SMEM, PER_NODE, 6, false>();
     }
+}
+
+int sm_count(int device)
+{
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v;
 }
 
 const void* pick_kernel(bool smem, bool per_node, int FT, bool slow)
@@ -653,15 +742,60 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
     return 0;
 }
 
-int launch_traj(TrajParams P, const LaunchPlan& plan, void* stream)
+int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* stream)
 {
     P.warps_per_group = plan.warps_per_group;
     P.image_smem_bytes = plan.image_in_smem ? P.L.bytes : 0u;
     const void* fn = pick_kernel(plan.image_in_smem, P.per_node != 0, P.L.fast_theta, P.L.slow_nodes > 0);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
     if (e != cudaSuccess) return (int)e;
+    cudaStream_t s = (cudaStream_t)stream;
+
+    // Persistent scheduling when one-CTA-per-group would leave the last wave
+    // partly empty (e.g. 512 groups on 148 SMs: 3.46 waves -> 86% busy).
+    const int64_t G = (P.n_chains + 31) / 32;
+    const int64_t total = P.burn_in + P.steps;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, plan.threads, plan.smem_bytes);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t resident = (int64_t)sm_count(device) * std::max(per_sm, 1);
+    bool persistent = false;
+    if (schedule == 2) {
+        persistent = total > 0;
+    } else if (schedule == 0 && G > resident && total >= 128) {
+        const int64_t waves = (G + resident - 1) / resident;
+        persistent = (double)G / (double)(waves * resident) < 0.97;
+    }
+    P.persistent = persistent ? 1 : 0;
+    int ctas = plan.ctas;
+    uint8_t* ws = nullptr;
+    if (persistent) {
+        // ~128 units per CTA keeps the last round's imbalance below 1%; a unit
+        // switch costs one group state save/restore (~10 KB through L2)
+        int64_t K = chunk_steps > 0 ? chunk_steps
+                                    : std::max<int64_t>(32, (total * G + resident * 128 - 1) / (resident * 128));
+        K = std::min(K, total);
+        P.n_groups = G;
+        P.chunk_steps = K;
+        P.total_units = G * ((total + K - 1) / K);
+        P.scratch_stride = P.n_pad + 8 * 32;
+        const size_t scratch_bytes = (size_t)G * (size_t)P.scratch_stride * 4;
+        const size_t ctl_bytes = 8 + (size_t)G * 4;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&ws), scratch_bytes + ctl_bytes + 16, s);
+        if (e != cudaSuccess) return (int)e;
+        P.work_ctr = reinterpret_cast<unsigned long long*>(ws);
+        P.done = reinterpret_cast<uint32_t*>(ws + 8);
+        P.scratch = reinterpret_cast<uint32_t*>(ws + ((ctl_bytes + 15) & ~(size_t)15));
+        e = cudaMemsetAsync(ws, 0, ctl_bytes, s);
+        if (e != cudaSuccess) return (int)e;
+        ctas = (int)std::min<int64_t>(resident, P.total_units);
+    }
     void* args[] = {&P};
-    e = cudaLaunchKernel(fn, dim3(plan.ctas), dim3(plan.threads), args, plan.smem_bytes, (cudaStream_t)stream);
+    e = cudaLaunchKernel(fn, dim3(ctas), dim3(plan.threads), args, plan.smem_bytes, s);
+    if (ws) {
+        const cudaError_t e2 = cudaFreeAsync(ws, s);
+        if (e == cudaSuccess) e = e2;
+    }
     return (int)e;
 }
 

@@ -102,6 +102,29 @@ def test_launch_shape_independence(pbn):
                     warps=warps)
         for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]:
             assert np.array_equal(g[k], ref[k]), (warps, k)
+    # persistent schedule: chunks straddle the burn-in end, batch and bit-word boundaries
+    for chunk, warps in [(1, 4), (7, 25), (33, 3), (299, 0), (1000, 8), (0, 0)]:
+        g = gpu_run(pm, model, pred, n_chains=200, steps=700, burn_in=300, seed=9, batch=64,
+                    warps=warps, schedule=2, chunk_steps=chunk)
+        for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]:
+            assert np.array_equal(g[k], ref[k]), ("persistent", chunk, warps, k)
+
+
+def test_persistent_schedule_large_group_count(pbn):
+    """More groups than resident CTAs (the C4 situation) with VECTOR and PER_NODE."""
+    model, pred = config_model("C2"), config_predicate("C2")
+    for per_node in (False, True):
+        pm = load(pbn, model, per_node)
+        a = gpu_run(pm, model, pred, n_chains=20000, steps=150, burn_in=50, seed=3, batch=16, schedule=1)
+        b = gpu_run(pm, model, pred, n_chains=20000, steps=150, burn_in=50, seed=3, batch=16, schedule=2,
+                    chunk_steps=37)
+        for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]:
+            assert np.array_equal(a[k], b[k]), (per_node, k)
+        ids = sample_chain_ids(20000, k=6, seed=1)
+        st, I, ws = oracle_run(model, pred, ids, steps=150, burn_in=50, seed=3, batch=16, per_node=per_node)
+        packed = pack_states(st)
+        for j, cid in enumerate(ids):
+            compare_chain(b, cid, packed[j], ws[j], 150, 16)
 
 
 def test_chain_split_and_step_split(pbn):
