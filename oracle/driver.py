@@ -1,0 +1,228 @@
+"""Oracle drivers: Algorithms 3, 4 and 5 of PAPER.md over the oracle simulator.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Every decision is taken from the stored 0/1 indicator sequences of each
+chain by definition (oracle/stats.py, oracle/skart.py); nothing is shared
+with the product's C++ driver.  Readings: Q7 boundary pairs,
+Q8 Gelman-Rubin details, Q9 Algorithm 4 garbles, Q11/Q12 Skart constants.
+
+Chain bookkeeping: `seq[c]` holds the indicator of chain c for every state
+after the Gelman-Rubin burn-in, i.e. states s_{psi+1}, s_{psi+2}, ... of the
+final GR length 2 psi (the GR window first, then every extension).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import sim
+from . import skart as osk
+from . import stats as ost
+
+
+@dataclass
+class RunResult:
+    estimate: float
+    rhat: float
+    psi: int
+    steps_per_chain: int
+    gr_iterations: int
+    extensions: int = 0
+    sample_size: int = 0
+    M: int = 0
+    N: int = 0
+    alpha: float = float("nan")
+    beta: float = float("nan")
+    ci_lo: float = float("nan")
+    ci_hi: float = float("nan")
+    trace: list = field(default_factory=list)
+
+
+class Chains:
+    """omega oracle chains advanced together; keeps each chain's indicator
+    history from a given start and its current state."""
+
+    def __init__(self, model, pred, seed: int, omega: int, threads: int = 8):
+        self.model, self.pred, self.seed, self.omega = model, pred, seed, omega
+        self.ids = np.arange(omega, dtype=np.uint32)
+        self.state = None
+        self.length = 0          # transitions simulated per chain
+        self.threads = threads
+
+    def advance(self, burn_in: int, steps: int) -> np.ndarray:
+        """Simulate burn_in + steps transitions; returns I [omega x steps]."""
+        init = self.state is None
+        st, I = sim.simulate(self.model, self.pred, self.seed, self.ids, self.length, burn_in, steps,
+                             init=init, state=self.state, threads=self.threads)
+        self.state = st
+        self.length += burn_in + steps
+        return I
+
+
+def generate_converged_chains(ch: Chains, psi0: int, threshold: float, max_steps: int):
+    """Algorithm 3.  Returns (psi, rhat, iterations, window
+    [omega x psi] = the last psi indicators of each chain) or raises."""
+    psi = psi0
+    window = ch.advance(psi, psi)          # trajectories of length 2 psi; last psi recorded
+    it = 0
+    while True:
+        it += 1
+        g = ost.gelman_rubin_windows(window) if np.any(window.var(axis=1) > 0) else None
+        rhat = g.rhat if g is not None else float("nan")
+        if g is not None and rhat < threshold:
+            return psi, rhat, it, window
+        if 4 * psi > max_steps:
+            raise RuntimeError("Gelman-Rubin did not converge within the step cap")
+        psi *= 2
+        window = ch.advance(0, psi)        # extend to 2 psi: the new window is the new segment
+
+
+def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold: float, r: float,
+                       s: float, eps: float, max_steps: int, threads: int = 8) -> RunResult:
+    """Algorithm 4 with reading Q9: extend by ceil((N - omega n)/omega)
+    while N > omega n; then if M > psi discard M - psi more initial elements of
+    every chain's sample, set psi := M and re-enter; stop when M <= psi."""
+    ch = Chains(model, pred, seed, omega, threads)
+    psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
+    seq = [[int(v) for v in window[c]] for c in range(omega)]   # per-chain sample (GR window first)
+    disc = 0                                         # elements discarded at the front
+    ext_count = 0
+    while True:
+        while True:
+            L = len(seq[0]) - disc
+            counts = ost.estimate_alpha_beta([np.asarray(x[disc:]) for x in seq]) if L >= 2 else None
+            ts = ost.two_state(*counts, r, s, eps) if counts is not None else None
+            if ts is not None and not ts.degenerate:
+                if ts.N <= omega * L:
+                    break
+                ext = -(-(ts.N - omega * L) // omega)
+            else:
+                ext = max(L, psi)
+            if ch.length + ext > max_steps:
+                raise RuntimeError("two-state sample exceeds the step cap")
+            I = ch.advance(0, ext)
+            for c in range(omega):
+                seq[c].extend(int(v) for v in I[c])
+            ext_count += 1
+        if ts.M > psi:
+            disc += ts.M - psi
+            psi = ts.M
+            disc = min(disc, len(seq[0]))
+            continue
+        break
+    L = len(seq[0]) - disc
+    total_ones = sum(sum(x[disc:]) for x in seq)
+    return RunResult(estimate=total_ones / (omega * L), rhat=rhat, psi=psi, steps_per_chain=ch.length,
+                     gr_iterations=it, extensions=ext_count, sample_size=omega * L, M=ts.M, N=ts.N,
+                     alpha=ts.alpha, beta=ts.beta)
+
+
+# --------------------------------------------------------------------------
+# Algorithm 5 (parallel Skart), constants of SPEC S:375 (reading Q11/Q12)
+# --------------------------------------------------------------------------
+SKEW_LIMIT = 4.0          # |B| <= 4 -> kappa = 1, else 16
+RANDOMNESS_LEVEL = 0.20   # von Neumann test, two-sided
+P_CEILING = 1024          # batch-count growth ceiling in the CI loop
+MAX_SKART_ITERS = 64
+
+
+def skewness(x: np.ndarray) -> float:
+    x = np.asarray(x, dtype=np.float64)
+    m = x.mean()
+    m2 = float(np.mean((x - m) ** 2))
+    if m2 == 0.0:
+        return float("nan")
+    return float(np.mean((x - m) ** 3)) / m2 ** 1.5
+
+
+def von_neumann_z(means: np.ndarray) -> float:
+    """Randomness statistic over per-chain sequences of batch means (SPEC
+    S:240) with successive differences taken only inside chains (reading
+    Q12): C = (mean squared successive difference over the m-1 within-chain
+    pairs) / (2 x sample variance of all means), z = (1-C) sqrt((m^2-1)/(m-2))
+    with m = pairs + 1.  For one chain this is the classical statistic.
+    Returns 0 (a pass) when there are fewer than 2 within-chain pairs: batch
+    means of different converged chains are independent."""
+    Y = np.asarray(means, dtype=np.float64)         # omega x k
+    omega, k = Y.shape
+    pairs = omega * (k - 1)
+    if pairs < 2:
+        return 0.0
+    flat = Y.ravel()
+    P = flat.size
+    mu = float(np.sum(flat)) / P
+    ss = float(np.sum((flat - mu) ** 2))
+    if ss == 0.0:
+        return float("inf")
+    msd = float(np.sum((Y[:, 1:] - Y[:, :-1]) ** 2)) / pairs
+    Cst = msd / (2.0 * ss / (P - 1))
+    m = pairs + 1
+    return (1.0 - Cst) * math.sqrt((m * m - 1.0) / (m - 2.0))
+
+
+def batch_sums(seq: list, start: int, kappa: int, per_chain: int) -> np.ndarray:
+    """Per-chain sums of per_chain consecutive kappa-batches from `start`."""
+    out = np.zeros((len(seq), per_chain), dtype=np.int64)
+    for c, x in enumerate(seq):
+        a = np.asarray(x[start:start + kappa * per_chain], dtype=np.int64)
+        out[c] = a.reshape(per_chain, kappa).sum(axis=1)
+    return out
+
+
+def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: float, h_star: float,
+                   alpha_conf: float, max_steps: int, threads: int = 8) -> RunResult:
+    ch = Chains(model, pred, seed, omega, threads)
+    psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
+    seq = [[int(v) for v in window[c]] for c in range(omega)]   # post-burn-in samples (skip first psi)
+
+    def ensure(per_chain_len: int):
+        need = per_chain_len - len(seq[0])
+        if need > 0:
+            if ch.length + need > max_steps:
+                raise RuntimeError("Skart sample exceeds the step cap")
+            I = ch.advance(0, need)
+            for c in range(omega):
+                seq[c].extend(int(v) for v in I[c])
+
+    z_pass = ost.inv_norm_cdf(1.0 - RANDOMNESS_LEVEL / 2.0)
+    eta = -(-1280 // omega) * omega                 # line 3
+    ensure(eta // omega)
+    allx = np.concatenate([np.asarray(x[:eta // omega]) for x in seq])
+    B = skewness(allx)                              # line 5, all samples
+    kappa = 1 if (not math.isnan(B) and abs(B) <= SKEW_LIMIT) else 16
+    p = -(-eta // omega) * omega                    # line 6
+    eta = kappa * p
+    d = 0
+    # lines 7-12: randomness test on spaced batch means
+    for _ in range(MAX_SKART_ITERS):
+        ensure(eta // omega)
+        per = p // omega
+        bs = batch_sums(seq, 0, kappa, per) / kappa
+        spaced = bs[:, ::d + 1]
+        z = von_neumann_z(spaced)
+        if abs(z) <= z_pass:
+            break
+        kappa = int(math.ceil(math.sqrt(2.0) * kappa))
+        d += 1
+        p = -(-p // omega) * omega
+        eta = kappa * p
+    # lines 13-21: CI loop on non-spaced batch means
+    for _ in range(MAX_SKART_ITERS):
+        ensure(eta // omega)
+        per = p // omega
+        ci = osk.ci_from_batches(batch_sums(seq, 0, kappa, per), kappa, alpha_conf)
+        if ci.H <= h_star:
+            return RunResult(estimate=ci.mu, rhat=rhat, psi=psi, steps_per_chain=ch.length,
+                             gr_iterations=it, sample_size=eta, ci_lo=ci.ci_lo, ci_hi=ci.ci_hi,
+                             trace=[(kappa, p, d)])
+        g = (ci.H / h_star) ** 2
+        new_eta = int(math.ceil(g * eta))
+        if p < P_CEILING:
+            p = min(P_CEILING, int(math.ceil(g * p)))
+        p = -(-p // omega) * omega
+        kappa = max(kappa, -(-new_eta // p))
+        eta = kappa * p
+    raise RuntimeError("Skart did not reach the precision within the iteration cap")

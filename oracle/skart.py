@@ -79,6 +79,8 @@ def ci_from_batches(batch_sums: np.ndarray, kappa: int, alpha_conf: float) -> Sk
     mu = float(np.sum(Y)) / P
     dev = Y - mu
     ss = float(np.sum(dev ** 2))
+    if ss == 0.0:   # all batch means equal: zero-width interval
+        return SkartCI(mu, 0.0, 0.0, float("nan"), mu, mu, 0.0, P)
     var = ss / (P - 1)
     D = dev.reshape(omega, per)
     lag = float(np.sum(D[:, :-1] * D[:, 1:]))

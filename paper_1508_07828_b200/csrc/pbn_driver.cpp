@@ -292,6 +292,121 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
         return PBN_OK;
     }
 
-    set_err(err, errlen, "Skart driver not available in this build yet");
-    return PBN_E_USAGE;
+    // ------------------- Algorithm 5 (readings Q11/Q12) ----------------------
+    // Declared Skart constants: skewness limit 4 (kappa 1 or 16),
+    // von Neumann randomness test at level 0.20 two-sided, kappa <- ceil(sqrt2
+    // kappa) and spacer d <- d + 1 on failure, batch-count ceiling 1024 in the
+    // CI loop.  Batches never straddle chains: p is a multiple of omega.
+    const double z_pass = pbn_inv_norm_cdf(1.0 - 0.20 / 2.0);
+    auto round_up = [omega](int64_t v) { return (v + omega - 1) / omega * omega; };
+    auto ensure = [&](int64_t per_chain_len) -> pbn_status {
+        const int64_t need = per_chain_len - ns;
+        if (need <= 0) return PBN_OK;
+        if (len + need > a->max_steps) return PBN_E_NOT_CONVERGED;
+        pbn_status s2 = launch(0, 0, need, ns, 0, nullptr);
+        if (s2 == PBN_OK) ns += need;
+        return s2;
+    };
+    std::vector<uint32_t> hbs;
+    // per-chain sums of `per` consecutive kappa-batches from the sample start
+    auto batches = [&](int64_t kappa, int64_t per) -> pbn_status {
+        if (!ws.ensure_batch(omega * per)) return PBN_E_NOMEM;
+        pbn_status s2 = pbn_recount(ws.bits, omega, ws.row_words, 0, kappa * per, kappa, nullptr, nullptr, nullptr,
+                                    nullptr, ws.batch, nullptr, ws.s);
+        if (s2 != PBN_OK) return s2;
+        hbs.resize((size_t)(omega * per));
+        if (cudaMemcpyAsync(hbs.data(), ws.batch, sizeof(uint32_t) * hbs.size(), cudaMemcpyDeviceToHost, ws.s) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(ws.s) != cudaSuccess)
+            return PBN_E_CUDA;
+        return PBN_OK;
+    };
+    auto fail = [&](pbn_status s2, const char* what) {
+        res->steps_per_chain = len;
+        set_err(err, errlen, "%s", what);
+        return s2;
+    };
+
+    int64_t eta = round_up(1280);  // Alg 5 line 3
+    if ((st = ensure(eta / omega)) != PBN_OK) return fail(st, "Skart: initial sample exceeds the step cap");
+    // skewness of all eta samples (line 5): for 0/1 data (1 - 2m) / sqrt(m (1 - m))
+    if ((st = pbn_recount(ws.bits, omega, ws.row_words, 0, eta / omega, 0, nullptr, nullptr, nullptr, nullptr,
+                          nullptr, ws.totals, ws.s)) != PBN_OK)
+        return st;
+    if ((st = read_counts(ws, &c, nullptr)) != PBN_OK) return st;
+    const double m1 = (double)c.S1 / (double)eta;
+    const bool skew_defined = m1 > 0.0 && m1 < 1.0;
+    const double skew = skew_defined ? (1.0 - 2.0 * m1) / std::sqrt(m1 * (1.0 - m1)) : NAN;
+    int64_t kappa = (skew_defined && std::fabs(skew) <= 4.0) ? 1 : 16;
+    int64_t p = round_up(eta);  // line 6
+    eta = kappa * p;
+    int64_t d = 0;
+    // lines 7-12: randomness (independence) test on spaced batch means
+    for (int iter = 0;; ++iter) {
+        if (iter >= 64) return fail(PBN_E_NOT_CONVERGED, "Skart: randomness test iteration cap");
+        if ((st = ensure(eta / omega)) != PBN_OK) return fail(st, "Skart: sample exceeds the step cap");
+        const int64_t per = p / omega;
+        if ((st = batches(kappa, per)) != PBN_OK) return st;
+        // spaced batch means: every (d+1)-th batch of each chain
+        const int64_t kept = (per + d) / (d + 1);
+        const int64_t pairs = omega * (kept - 1);
+        bool pass = true;
+        if (pairs >= 2) {
+            const int64_t P = omega * kept;
+            long double sum = 0.0L;
+            for (int64_t ch = 0; ch < omega; ++ch)
+                for (int64_t k = 0; k < kept; ++k) sum += hbs[(size_t)(ch * per + k * (d + 1))];
+            const double mu = (double)(sum / (long double)P) / (double)kappa;
+            double ss = 0.0, sd = 0.0;
+            for (int64_t ch = 0; ch < omega; ++ch)
+                for (int64_t k = 0; k < kept; ++k) {
+                    const double y = (double)hbs[(size_t)(ch * per + k * (d + 1))] / (double)kappa;
+                    ss += (y - mu) * (y - mu);
+                    if (k > 0) {
+                        const double yp = (double)hbs[(size_t)(ch * per + (k - 1) * (d + 1))] / (double)kappa;
+                        sd += (y - yp) * (y - yp);
+                    }
+                }
+            if (ss == 0.0) {
+                pass = false;
+            } else {
+                const double Cst = (sd / (double)pairs) / (2.0 * ss / (double)(P - 1));
+                const double mm = (double)(pairs + 1);
+                const double z = (1.0 - Cst) * std::sqrt((mm * mm - 1.0) / (mm - 2.0));
+                pass = std::fabs(z) <= z_pass;
+            }
+        }
+        if (pass) break;
+        kappa = (int64_t)std::ceil(std::sqrt(2.0) * (double)kappa);
+        d += 1;
+        p = round_up(p);
+        eta = kappa * p;
+    }
+    // lines 13-21: CI loop on non-spaced batch means (no further discarding)
+    for (int iter = 0;; ++iter) {
+        if (iter >= 64) return fail(PBN_E_NOT_CONVERGED, "Skart: precision iteration cap");
+        if ((st = ensure(eta / omega)) != PBN_OK) return fail(st, "Skart: sample exceeds the step cap");
+        const int64_t per = p / omega;
+        if ((st = batches(kappa, per)) != PBN_OK) return st;
+        pbn_skart_ci ci;
+        st = pbn_skart_ci_from_batches(hbs.data(), omega, per, kappa, a->alpha_conf, &ci);
+        if (st != PBN_OK && st != PBN_E_DEGENERATE) return st;
+        if (ci.H <= a->h_star) {
+            res->estimate = ci.mu;
+            res->ci_lo = ci.ci_lo;
+            res->ci_hi = ci.ci_hi;
+            res->psi = psi;
+            res->sample_size = eta;
+            res->steps_per_chain = len;
+            res->M = kappa;  // report the final batch size and count in M / N
+            res->N = p;
+            return PBN_OK;
+        }
+        const double g = (ci.H / a->h_star) * (ci.H / a->h_star);
+        const int64_t new_eta = (int64_t)std::ceil(g * (double)eta);
+        if (p < 1024) p = std::min<int64_t>(1024, (int64_t)std::ceil(g * (double)p));
+        p = round_up(p);
+        kappa = std::max(kappa, (new_eta + p - 1) / p);
+        eta = kappa * p;
+    }
 }

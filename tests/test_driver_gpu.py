@@ -1,0 +1,93 @@
+"""GPU: the library's host driver (pbn_run: Algorithm 3 then 4 or 5) vs the
+oracle drivers (oracle/driver.py) on the same seeded inputs.
+
+Integer decisions (psi, iterations, extensions, sample sizes, M, N, batch
+size and count) must be identical; fp64 statistics agree within 1e-9
+relative (BASELINE north_star).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import driver as odr
+from workloads import CONFIGS, Predicate, config_model, config_predicate, random_pbn
+
+pytestmark = pytest.mark.gpu
+REL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def pbn():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1508_07828_b200 as pbn
+    return pbn
+
+
+def close(a, b, rel=REL):
+    return math.isclose(a, b, rel_tol=rel, abs_tol=1e-300)
+
+
+def run_both_two_state(pbn, model, pred, omega, psi0, thr, r, s, eps, seed, max_steps=1 << 22):
+    pm = pbn.pbn_load(model)
+    st, res, err = pbn.pbn_run(pm, method=0, omega=omega, psi0=psi0, rhat_threshold=thr, r=r, s=s, eps=eps,
+                               seed=seed, pred=pred, max_steps=max_steps)
+    assert st == 0, err
+    o = odr.parallel_two_state(model, pred, seed, omega, psi0, thr, r, s, eps, max_steps, threads=16)
+    return res, o
+
+
+def check_two_state(res, o):
+    assert (res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain) == (
+        o.psi, o.gr_iterations, o.extensions, o.sample_size, o.steps_per_chain)
+    assert (res.M, res.N) == (o.M, o.N)
+    assert close(res.rhat, o.rhat) and close(res.alpha, o.alpha) and close(res.beta, o.beta)
+    assert close(res.estimate, o.estimate, 1e-12)
+
+
+def test_two_state_driver_C1_model(pbn):
+    model, pred = config_model("C1"), config_predicate("C1")
+    res, o = run_both_two_state(pbn, model, pred, omega=8, psi0=500, thr=1.1, r=0.01, s=0.95, eps=1e-10,
+                                seed=1)
+    check_two_state(res, o)
+
+
+def test_two_state_driver_burn_in_recheck(pbn):
+    """A slowly mixing model with a tiny psi0 so that M > psi forces the
+    Algorithm 4 burn-in re-check (discard + recount)."""
+    nodes = [[([0], [0, 1], 1.0)], [([0, 1], [0, 1, 1, 1], 0.9), ([], [0], 0.1)]]
+    from workloads import model_from_lists
+    model = model_from_lists(2, 0.002, nodes)
+    pred = Predicate(np.array([1], np.uint16), np.array([1], np.uint8))
+    res, o = run_both_two_state(pbn, model, pred, omega=4, psi0=8, thr=1.5, r=0.02, s=0.95, eps=1e-10, seed=7)
+    check_two_state(res, o)
+
+
+def test_two_state_driver_C2_config(pbn):
+    """BASELINE C2: 1024 chains, psi0 = 1000, R-hat < 1.1, r = 0.01, s = 0.95."""
+    c = CONFIGS["C2"]
+    x = c.extra
+    res, o = run_both_two_state(pbn, config_model("C2"), config_predicate("C2"), omega=c.chains,
+                                psi0=x["psi0"], thr=x["rhat_threshold"], r=x["r"], s=x["s"], eps=x["eps"],
+                                seed=c.sim_seed)
+    check_two_state(res, o)
+
+
+@pytest.mark.parametrize("omega,seed", [(8, 3), (3, 5), (64, 2)])
+def test_skart_driver(pbn, omega, seed):
+    model = random_pbn(12, 1, 3, 1, 3, 0.02, seed=seed)
+    pred = Predicate(np.array([0, 5], np.uint16), np.array([1, 0], np.uint8))
+    pm = pbn.pbn_load(model)
+    st, res, err = pbn.pbn_run(pm, method=1, omega=omega, psi0=256, rhat_threshold=1.1, h_star=0.01,
+                               alpha_conf=0.05, seed=seed, pred=pred, max_steps=1 << 22)
+    assert st == 0, err
+    o = odr.parallel_skart(model, pred, seed, omega, 256, 1.1, 0.01, 0.05, 1 << 22, threads=16)
+    kappa, p, d = o.trace[-1]
+    assert (res.psi, res.gr_iterations, res.sample_size, res.steps_per_chain) == (
+        o.psi, o.gr_iterations, o.sample_size, o.steps_per_chain)
+    assert (res.M, res.N) == (kappa, p)
+    for a, b in [(res.estimate, o.estimate), (res.ci_lo, o.ci_lo), (res.ci_hi, o.ci_hi), (res.rhat, o.rhat)]:
+        assert close(a, b), (a, b)
+    assert res.ci_lo <= res.estimate <= res.ci_hi
