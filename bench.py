@@ -171,6 +171,49 @@ def workload_config(args, cfg, model) -> dict:
 
 
 # --------------------------------------------------------------------------
+def run_sweep(args, cfg, model, pred):
+    """BASELINE config C5: node-updates/s and ALU-roofline fraction versus chain
+    count (one JSON line per chain count; not the driver's bench line)."""
+    import torch
+    import paper_1508_07828_b200 as pbn
+    torch.cuda.set_device(0)
+    pm = pbn.pbn_load(model)
+    ops = algorithmic_alu_ops(model)
+    peak = SM_COUNT_B200 * ALU_LANES_PER_CLK_PER_SM * 1965.0 * 1e6 / 1e12
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    sweep = cfg.extra.get("chain_sweep", (1, 64, 1024, 16384))
+    for chains in sweep:
+        out = pbn.alloc_outputs(pm, chains, args.window, batch=cfg.batch, emit_bits=True)
+
+        def one():
+            pbn.pbn_simulate(pm, out, n_chains=chains, steps=args.window, burn_in=args.burn_in,
+                             batch=cfg.batch, seed=cfg.sim_seed, pred=pred, init=True, emit_bits=True,
+                             stream=stream)
+        for _ in range(args.warmup):
+            one()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(args.steps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            one()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        t = statistics.median(ms) / 1e3
+        nu = chains * (args.burn_in + args.window) * model.n
+        print(json.dumps({"sweep": cfg.key, "chains": chains, "n": model.n,
+                          "steps_per_chain": args.burn_in + args.window,
+                          "node_updates_per_s": nu / t, "chain_steps_per_s": chains * (args.burn_in + args.window) / t,
+                          "ms": t * 1e3, "roofline_frac_alu": nu * ops / t / 1e12 / peak,
+                          "image_bytes": int(pm.info.image_bytes)}), flush=True)
+        del out
+    pm.close()
+
+
+# --------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -187,6 +230,7 @@ def main():
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=0, help="0 auto, 1 CTA per group, 2 persistent")
     ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
+    ap.add_argument("--sweep", action="store_true", help="C5 chain-count sweep (one line per count)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
@@ -201,6 +245,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
+    if args.sweep:
+        if args.config == "C4":
+            args.config = "C5"
+        cfg = CONFIGS[args.config]
+        args.burn_in = cfg.burn_in if args.burn_in is None else args.burn_in
+        args.window = cfg.steps if args.window is None else args.window
+        run_sweep(args, cfg, config_model(args.config), config_predicate(args.config))
+        return
     if args.impl == "reference":
         run_reference(args, cfg, model, pred, rank)
         return

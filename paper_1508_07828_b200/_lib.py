@@ -13,6 +13,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpbnsim.so")
+# experiments only: an alternative in-tree build (e.g. libpbnsim_u16.so) by file name
+if os.environ.get("PBN_LIB_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), os.environ["PBN_LIB_VARIANT"])
 
 # status codes
 PBN_OK = 0

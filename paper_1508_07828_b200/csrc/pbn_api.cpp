@@ -232,7 +232,8 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
         uint32_t w3 = 0;  // nrec[i].w, written last (B.alloc may move the buffer)
         if (fast[i]) {
             const int32_t tm = FT;  // every fast function is padded to the model-wide FT
-            const uint32_t off_desc = B.alloc((size_t)pbn::kDescBytes * ell, 8);
+            const uint32_t ds = pbn::desc_bytes(FT);
+            const uint32_t off_desc = B.alloc((size_t)ds * ell, 16);
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;
                 const int32_t theta = d->par_off[f + 1] - d->par_off[f];
@@ -240,14 +241,19 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                 uint64_t T = 0;
                 for (uint32_t idx = 0; idx < (1u << tm); ++idx)
                     T |= (uint64_t)table_bit(d, f, idx >> (tm - theta)) << idx;
-                const uint32_t off = off_desc + pbn::kDescBytes * (uint32_t)j;
+                uint32_t* w = B.u32(off_desc + ds * (uint32_t)j);
                 // stored bit-reversed per word: entry e at bit 31 - (e & 31)
-                B.u32(off)[0] = reverse_bits((uint32_t)T);
-                B.u32(off)[1] = reverse_bits((uint32_t)(T >> 32));
-                // padded parent list, MSB first; dummies read node 0
-                uint16_t* par = B.u16(off + 8u);
-                for (int32_t m = 0; m < tm; ++m)
-                    par[m] = (uint16_t)(m < theta ? 4u * d->parents[d->par_off[f] + m] : 0u);
+                int k = 0;
+                w[k++] = reverse_bits((uint32_t)T);
+                if (tm == 6) w[k++] = reverse_bits((uint32_t)(T >> 32));
+                // padded parent list, MSB first, as state-relative byte offsets;
+                // dummies read node 0
+                auto par = [&](int32_t m) { return pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u); };
+                for (int32_t m = 0; m < tm; ++m) {
+                    // relocated by the state base in shared memory (flag kRelocState)
+                    reloc.push_back((off_desc + ds * (uint32_t)j + 4u * (uint32_t)k) | pbn::kRelocState);
+                    w[k++] = par(m);
+                }
             }
             w3 = off_desc;
         } else {
@@ -261,9 +267,8 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                 const int32_t words = d->tbl_off[f + 1] - d->tbl_off[f];
                 const uint32_t off_t = B.alloc(4u * words, 4);
                 for (int32_t w = 0; w < words; ++w) B.u32(off_t)[w] = d->tables[d->tbl_off[f] + w];
-                const uint32_t off_p = B.alloc(2u * (size_t)std::max(theta, 1), 4);
-                for (int32_t m = 0; m < theta; ++m)
-                    B.u16(off_p)[m] = (uint16_t)(4u * d->parents[d->par_off[f] + m]);
+                const uint32_t off_p = B.alloc(4u * (size_t)std::max(theta, 1), 4);
+                for (int32_t m = 0; m < theta; ++m) B.u32(off_p)[m] = pbn::state_off(d->parents[d->par_off[f] + m]);
                 uint32_t* gd = B.u32(off_gd + 16u * j);
                 gd[0] = off_t;
                 gd[1] = (uint32_t)theta;
@@ -405,7 +410,8 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     P->nquads = (m->L.n + 3) / 4;
     P->n_pad = (m->L.n + 3) & ~3;
     P->state_words = (m->L.n + 31) / 32;
-    P->group_words = (P->per_node ? 2 : 3) * P->n_pad + 32;
+    // group state (2 interleaved buffers) + gamma words + [32] any words, 16-aligned
+    P->group_words = ((P->per_node ? 2 : 3) * P->n_pad + 32 + 3) & ~3;
     // Philox4x32-10 key schedule: round r uses (k0 + r W0, k1 + r W1), key = seed
     for (uint32_t r = 0; r < 10; ++r) {
         P->rk[2 * r + 0] = (uint32_t)a->seed + r * 0x9E3779B9u;

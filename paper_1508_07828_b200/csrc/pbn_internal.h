@@ -10,10 +10,10 @@
 //       E_k  selection thresholds of reading Q3 as E_k = D_k - 1: the
 //            selected function is j = #{k : u > E_k}; unused = 0xFFFFFFFF
 //       w    FAST node (ell <= 4, theta_max <= 6): offset of the node's first
-//            fast descriptor (8-aligned, low 3 bits 0)
+//            fast descriptor (16-aligned, low 4 bits 0)
 //            SLOW node (anything else): offset of its slow record | 7
-//   fast descriptor (24 bytes, per function of a fast node, consecutive)
-//            {t0, t1, par[0..FT-1] (u16)}
+//   fast descriptor (desc_bytes(FT) bytes, per function of a fast node,
+//            consecutive): u32 words {t0, [t1 if FT == 6], a[0..FT-1]}
 //       every fast function is PADDED to the model-wide fast width FT (the
 //       largest theta over fast nodes, 3 <= FT <= 6): its parent list is
 //       extended with dummy parents that the table ignores
@@ -23,22 +23,34 @@
 //       t0,t1  the padded 2^FT-entry table, entries 0-31 in t0 and 32-63 in t1,
 //              each word BIT-REVERSED (entry e at bit 31 - (e & 31)) so the
 //              kernel reads an entry as the sign bit of (word << (e & 31))
-//       par    (parent node * 4) for m < FT, MSB first (parents[0] first,
-//              reading Q5); the pad entries read node 0
+//       a[m]   state_off(parent m), MSB first (parents[0] first, reading Q5);
+//              the pad entries read node 0
 //   slow record (uint4, per slow node)  {thr, ell, gdesc, 0}
 //       thr    offset of ell-1 u32 thresholds E_1..E_{ell-1}
 //       gdesc  offset of ell generic descriptors
 //   generic descriptor (uint4)          {toff, theta, poff, 0}
-//       toff   offset of the ceil(2^theta/32) table words; poff: u16 parent list
-//              (node*4), parents[0] first (MSB, reading Q5)
+//       toff   offset of the ceil(2^theta/32) table words; poff: u32 list of
+//              state_off(parent), parents[0] first (MSB, reading Q5)
 //   relocation list (u32, stored after the image in device memory, not staged)
-//       byte offsets of every offset-valued word above (nrec.w, thr, gdesc,
-//       toff, poff).  After staging, each CTA adds its shared-memory
-//       base to those words, so the hot loop uses absolute shared addresses.
+//       byte offsets of every image-offset-valued word above (nrec.w, thr,
+//       gdesc, toff, poff) and, flagged with kRelocState, of every fast
+//       parent offset a[m].  After staging, each CTA adds its shared-memory
+//       image base (resp. its group-state base) to those words, so the hot
+//       loop uses absolute shared addresses: a parent's state word is one
+//       LDS [a[m] + 16 b].  (Global-image launches add the state base per load.)
+//
+// Group state in shared memory (one 32-chain group per CTA): BIT-SLICED,
+// word (node i, buffer b) holds node i of the 32 chains (bit l = lane l) at
+//     state base + state_off(i) + 16 b,   state_off(i) = 32 (i >> 2) + 4 (i & 3)
+// i.e. the two buffers are interleaved at 4-node-quad granularity: a quad's
+// four words are contiguous in each buffer (one 16-byte commit) and the
+// buffer is an immediate offset on every state load.
 //
 // The thresholds are the product's own computation of reading Q3
 // (pbn_api.cpp build_image); nothing here is shared with oracle/.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace pbn {
@@ -46,7 +58,12 @@ namespace pbn {
 constexpr int kMaxPred = 16;
 constexpr int kMaxWarpsPerCta = 32;
 constexpr uint32_t kSlowNode = 7;   // nrec.w low bits marking a slow node
-constexpr uint32_t kDescBytes = 24;  // fast descriptor stride
+constexpr uint32_t kRelocState = 0x80000000u;  // relocation entry: add the state base
+// fast descriptor stride for fast width FT: t0 (+t1 when FT == 6) + FT offsets,
+// rounded up to 16 bytes
+__host__ __device__ constexpr uint32_t desc_bytes(int FT) { return FT == 3 ? 16u : 32u; }
+// byte offset of node i's word in buffer 0 of the group state
+__host__ __device__ constexpr uint32_t state_off(uint32_t i) { return 32u * (i >> 2) + 4u * (i & 3u); }
 constexpr int kFastMaxTheta = 6;
 constexpr int kFastMinTheta = 3;
 constexpr int kFastMaxEll = 4;

@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 
 #include "pbn_internal.h"
 
@@ -226,6 +227,7 @@ struct Img {
 };
 
 // Generic path for nodes outside the fast shape (ell > 4 or theta_max > 6).
+// `old` = address of buffer-0 word of node 0 plus the old buffer's offset.
 template <bool SMEM>
 __device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w, uint32_t u, uint32_t old,
                                                uint32_t rot)
@@ -236,7 +238,7 @@ __device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w,
     const uint4 gd = img.ld128(sr.z + 16u * j);  // {toff, theta, poff, 0}
     uint32_t idx = 0;
     for (uint32_t m = 0; m < gd.y; ++m) {
-        const uint32_t off = img.ld16(gd.z + 2u * m);
+        const uint32_t off = img.ld32(gd.z + 4u * m);
         const uint32_t wv = lds32(old + off);
         idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
     }
@@ -244,16 +246,8 @@ __device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w,
     return (tw >> (idx & 31u)) & 1u;
 }
 
-// One node of one step for the warp's 32 chains (A4-A7).  Returns the gamma word.
-// Split a u32 holding two u16 parent offsets (low half = first) on the FMA
-// pipe: hi = x >> 16 as a mul-high, lo = x - hi * 2^16 as a mul-add.
-__device__ __forceinline__ void split_pair(uint32_t x, uint32_t& lo, uint32_t& hi)
-{
-    asm("mul.hi.u32 %1, %2, 65536;\n\tmad.lo.u32 %0, %1, 0xFFFF0000, %2;" : "=r"(lo), "=r"(hi) : "r"(x));
-}
-
 // idx += B when this lane's bit of the parent word is set: one LOP3 producing a
-// predicate (ALU pipe) and one predicated add (FMA pipe).
+// predicate (ALU pipe) and one predicated add.
 template <uint32_t B>
 __device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t lmask)
 {
@@ -265,60 +259,69 @@ __device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t 
 
 // One node of one step for the warp's 32 chains (A4-A7): returns the node's
 // new state word (bit l = chain of lane l) and its gamma word in *gw_out.
-template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
+//   sb   state base (shared address of buffer-0 word of node 0; uniform)
+//   OB   byte offset of the OLD buffer (0 or 16, compile time)
+template <bool SMEM, bool PER_NODE, int FT, bool SLOW, uint32_t OB>
 __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec_addr, uint32_t i, uint32_t u,
-                                              uint32_t Tp, uint32_t old, uint32_t lmask, uint32_t rot,
+                                              uint32_t Tp, uint32_t sb, uint32_t lmask, uint32_t rot,
                                               uint32_t& gw_out)
 {
+    constexpr uint32_t DS = desc_bytes(FT);
     const uint4 rec = img.ld128(rec_addr);
     const uint32_t gw = __ballot_sync(FULL, u < Tp);  // gamma_i(t) = 1 (A4)
     uint32_t bit;
     if (!SLOW || (rec.w & 7u) != kSlowNode) {
         // A5: descriptor of function j = #{k : u > E_k}
         uint32_t dp = rec.w;
-        if (u > rec.x) dp += kDescBytes;
-        if (u > rec.y) dp += kDescBytes;
-        if (u > rec.z) dp += kDescBytes;
-        const uint2 t = img.ld64(dp);  // padded table (bit-reversed words)
-        // FT padded parent offsets, MSB first, two per u32
-        uint32_t off[6];
+        if (u > rec.x) dp += DS;
+        if (u > rec.y) dp += DS;
+        if (u > rec.z) dp += DS;
+        // descriptor words {t0, [t1], a[0..FT-1]}: table word(s), then the FT
+        // padded parents' state offsets, MSB first
+        uint32_t tw0, tw1 = 0, a[6];
         {
-            uint32_t w01, w23 = 0, w45 = 0;
-            if (FT > 2) {
-                const uint2 a = img.ld64(dp + 8u);
-                w01 = a.x;
-                w23 = a.y;
+            const uint4 d0 = img.ld128(dp);
+            if (FT == 6) {
+                const uint4 d1 = img.ld128(dp + 16u);
+                tw0 = d0.x; tw1 = d0.y; a[0] = d0.z; a[1] = d0.w;
+                a[2] = d1.x; a[3] = d1.y; a[4] = d1.z; a[5] = d1.w;
+            } else if (FT == 5) {
+                const uint2 d1 = img.ld64(dp + 16u);
+                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1.x; a[4] = d1.y; a[5] = 0;
+            } else if (FT == 4) {
+                const uint32_t d1 = img.ld32(dp + 16u);
+                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1; a[4] = a[5] = 0;
             } else {
-                w01 = img.ld32(dp + 8u);
+                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = a[4] = a[5] = 0;
             }
-            if (FT > 4) w45 = img.ld32(dp + 16u);
-            split_pair(w01, off[0], off[1]);
-            split_pair(w23, off[2], off[3]);
-            split_pair(w45, off[4], off[5]);
         }
         // A6: gather: parent k contributes bit (FT-1-k) of the table index when
         // bit `lane` of its state word is set (LOP3 -> predicate, predicated add)
         // FT = 6: the first (most significant) parent picks the table word
         // (entries 32-63 in t1), the other five index within it
-        uint32_t tw = t.x;
-        if (FT == 6) tw = (lds32_state(old + off[0]) & lmask) ? t.y : t.x;
+        // parent state word: absolute (relocated) address in shared-image
+        // launches, state-relative otherwise
+#define SB(x) (SMEM ? (x) : sb + (x))
+        uint32_t tw = tw0;
+        if (FT == 6) tw = (lds32_state(SB(a[0]) + OB) & lmask) ? tw1 : tw0;
         constexpr int S = FT == 6 ? 1 : 0;  // first parent handled above
         constexpr int R = FT - S;          // parents indexing within the word
         uint32_t idx = 0;
-        if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(old + off[S + 0]), lmask);
-        if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(old + off[S + 1]), lmask);
-        if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(old + off[(S + 2) % 6]), lmask);
-        if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(old + off[(S + 3) % 6]), lmask);
-        if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(old + off[(S + 4) % 6]), lmask);
+        if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(SB(a[S + 0]) + OB), lmask);
+        if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(SB(a[S + 1]) + OB), lmask);
+        if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(SB(a[(S + 2) % 6]) + OB), lmask);
+        if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(SB(a[(S + 3) % 6]) + OB), lmask);
+        if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(SB(a[(S + 4) % 6]) + OB), lmask);
         // the table words are stored bit-REVERSED (entry e at bit 31 - (e & 31)),
         // so the entry is the sign bit of the word shifted left by idx
         bit = (uint32_t)((int32_t)(tw << idx) < 0);
+#undef SB
     } else {
-        bit = slow_node_bit<SMEM>(img, rec.w, u, old, rot);
+        bit = slow_node_bit<SMEM>(img, rec.w, u, sb + OB, rot);
     }
     uint32_t nb = __ballot_sync(FULL, bit != 0u);  // commit (A7)
     if (PER_NODE) {
-        const uint32_t ow = lds32_state(old + 4u * i);
+        const uint32_t ow = lds32_state(sb + state_off(i) + OB);
         nb = (nb & ~gw) | (~ow & gw);
     }
     gw_out = gw;
@@ -336,7 +339,10 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
     const int lane = tid & 31;
     const int W = P.warps_per_group;
     const int n = P.n;
-    const uint32_t sbase = smem_u32(smem);
+    // dynamic shared memory: [group state | gamma words | any words] then the
+    // staged image (16-aligned) -- the state sits at the window's dynamic base
+    const uint32_t gbase = smem_u32(smem);                   // state base
+    const uint32_t sbase = gbase + 4u * (uint32_t)P.group_words;  // image base
 
     // ---- A1: stage the model image into shared memory (bulk async copy) ----
     Img<SMEM> img;
@@ -367,9 +373,11 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             : "memory");
         // relocate: offsets -> absolute shared addresses of this CTA's copy
         const uint32_t* rel = reinterpret_cast<const uint32_t*>(P.image + P.L.reloc_off);
+        const uint32_t state_base = gbase;
         for (int k = tid; k < P.L.reloc_count; k += blockDim.x) {
-            const uint32_t a = sbase + __ldg(rel + k);
-            sts32(a, lds32(a) + sbase);
+            const uint32_t e = __ldg(rel + k);
+            const uint32_t a = sbase + (e & ~kRelocState);
+            sts32(a, lds32(a) + ((e & kRelocState) ? state_base : sbase));
         }
         __syncthreads();
     }
@@ -379,7 +387,6 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
     const uint32_t rot = 31u - (uint32_t)lane;       // rotate-left amount: bit `lane` -> bit 31
     const uint32_t lmask = 1u << lane;               // this chain's bit in a state word
 
-    const uint32_t gbase = sbase + P.image_smem_bytes;
     const uint32_t gam = gbase + 8u * P.n_pad;   // VECTOR: gamma words
     const uint32_t anyw = gbase + 4u * (PER_NODE ? 2 : 3) * P.n_pad;  // [W]
     const uint32_t nrec = SMEM ? sbase : 0u;     // node records start the image
@@ -436,8 +443,9 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         const int64_t chain_local = group * 32 + lane;
         const bool valid = chain_local < P.n_chains;
         const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
-        uint32_t bufA = gbase;                  // current state s_{t-1}
-        uint32_t bufB = gbase + 4u * P.n_pad;   // next state s_t
+        // state buffers: word (i, b) at gbase + state_off(i) + 16 b; every
+        // chunk starts from buffer 0, `cur` tracks the newest buffer
+        uint32_t cur = 0;
         uint32_t* scr = P.scratch + group * (int64_t)P.scratch_stride;  // persistent only
 
         // ---- per-lane statistics (warp 0) ----
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         if (!first_chunk) {
             // resume: bit-sliced state words and warp-0 counters from scratch
             __syncthreads();
-            for (int i = tid; i < n; i += blockDim.x) sts32(bufA + 4u * i, __ldcg(scr + i));
+            for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr + i));
             if (wg == 0) {
                 const uint32_t* st = scr + P.n_pad + 8 * lane;
                 c1 = __ldcg(st + 0);
@@ -468,7 +476,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                     const int i = 4 * q + k;
                     if (i < n) {
                         const uint32_t wv = __ballot_sync(FULL, (rr[k] >> 31) != 0u);
-                        if (leader) sts32(bufA + 4u * i, wv);
+                        if (leader) sts32(gbase + state_off(i), wv);
                     }
                 }
             }
@@ -479,62 +487,68 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
                     const int i = 32 * b + k;
                     if (i >= n) break;
                     const uint32_t wv = __ballot_sync(FULL, (v >> k) & 1u);
-                    if (leader) sts32(bufA + 4u * i, wv);
+                    if (leader) sts32(gbase + state_off(i), wv);
                 }
             }
         }
         __syncthreads();
 
-    // one synchronous step s_{t-1} (bufA) -> s_t (bufB); the step loop below is
-    // unrolled by two with the buffer roles fixed in each half, so the buffer
-    // bases stay loop-invariant (uniform registers, [R+UR] addressing)
-    auto step = [&](const int64_t r, const uint32_t bufA, const uint32_t bufB) {
+    // one synchronous step s_{t-1} (buffer OB) -> s_t (buffer NB = 16 - OB);
+    // the step loop below is unrolled by two with the buffer roles fixed in
+    // each half, so every state access is [R + UR + imm]
+    auto step = [&](const int64_t r, auto ob_c) {
+        constexpr uint32_t OB = decltype(ob_c)::value;
+        constexpr uint32_t NB = 16u - OB;
         const uint64_t t = (uint64_t)(P.step0 + r);
         const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
         uint32_t any = 0;
         const PhiloxStep ps = philox_step(chain, t_lo, t_hi, P.rk);
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
-        // software pipeline: the next quad's Philox words are computed while
-        // this quad's nodes gather (independent instruction streams)
-        uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
-        for (int q = q0; q < qf; ++q) {
-            const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
+        // one full quad: four independent nodes, then one 16-byte store commits
+        // them (and their gamma words if any)
+        auto quad = [&](const int q, const uint4 rw) {
             const uint32_t i0 = 4u * (uint32_t)q;
             const uint32_t ra = nrec + 16u * i0;
             // the quad's four nodes are independent: compute all, then one
             // 16-byte store commits them (and their gamma words if any)
             uint32_t g0, g1, g2, g3;
-            const uint32_t w0 = node_word<SMEM, PER_NODE, FT, SLOW>(img, ra, i0, rw.x, Tp, bufA, lmask, rot, g0);
+            const uint32_t w0 =
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra, i0, rw.x, Tp, gbase, lmask, rot, g0);
             const uint32_t w1 =
-                node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u, i0 + 1, rw.y, Tp, bufA, lmask, rot, g1);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 16u, i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
             const uint32_t w2 =
-                node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 32u, i0 + 2, rw.z, Tp, bufA, lmask, rot, g2);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 32u, i0 + 2, rw.z, Tp, gbase, lmask, rot, g2);
             const uint32_t w3 =
-                node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 48u, i0 + 3, rw.w, Tp, bufA, lmask, rot, g3);
-            sts128_if(bufB + 4u * i0, w0, w1, w2, w3, lead);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 48u, i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
+            sts128_if(gbase + 32u * (uint32_t)q + NB, w0, w1, w2, w3, lead);
             if (!PER_NODE) {
                 const uint32_t g = g0 | g1 | g2 | g3;
                 any |= g;
                 // gamma words only when nonzero (rare); the fixup clears them
                 sts128_if(gam + 4u * i0, g0, g1, g2, g3, g & lead);
             }
+        };
+        // software pipeline: the next quad's Philox words are computed while
+        // this quad's nodes gather (independent instruction streams)
+        uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
+        for (int q = q0; q < qf; ++q) {
+            const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
+            quad(q, rw);
             rw = rn;
         }
         if (qf < q1) {  // ragged last quad (n % 4 != 0), node by node
-            {
-                const int q = qf;
-                const uint32_t i0 = 4u * (uint32_t)q;
-                const uint32_t ra = nrec + 16u * i0;
-                const uint32_t rr[4] = {rw.x, rw.y, rw.z, rw.w};
-                for (uint32_t k = 0; k < 4 && (int)(i0 + k) < n; ++k) {
-                    uint32_t gk;
-                    const uint32_t wk = node_word<SMEM, PER_NODE, FT, SLOW>(img, ra + 16u * k, i0 + k, rr[k], Tp,
-                                                                            bufA, lmask, rot, gk);
-                    sts32_if(bufB + 4u * (i0 + k), wk, lead);
-                    if (!PER_NODE) {
-                        any |= gk;
-                        sts32_if(gam + 4u * (i0 + k), gk, gk & lead);
-                    }
+            const int q = qf;
+            const uint32_t i0 = 4u * (uint32_t)q;
+            const uint32_t ra = nrec + 16u * i0;
+            const uint32_t rr[4] = {rw.x, rw.y, rw.z, rw.w};
+            for (uint32_t k = 0; k < 4 && (int)(i0 + k) < n; ++k) {
+                uint32_t gk;
+                const uint32_t wk = node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 16u * k, i0 + k, rr[k], Tp,
+                                                                            gbase, lmask, rot, gk);
+                sts32_if(gbase + 32u * (uint32_t)q + NB + 4u * k, wk, lead);
+                if (!PER_NODE) {
+                    any |= gk;
+                    sts32_if(gam + 4u * (i0 + k), gk, gk & lead);
                 }
             }
         }
@@ -546,20 +560,20 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             if (M) {
                 const int lo = 4 * q0, hi = min(4 * q1, n);
                 for (int i = lo + lane; i < hi; i += 32) {
-                    const uint32_t a = 4u * (uint32_t)i;
-                    const uint32_t gmm = lds32(gam + a);
-                    if (gmm) sts32(gam + a, 0u);  // keep the gamma buffer all-zero
-                    const uint32_t f = lds32(bufB + a), o = lds32(bufA + a);
-                    sts32(bufB + a, (f & ~M) | ((o ^ gmm) & M));
+                    const uint32_t gmm = lds32(gam + 4u * (uint32_t)i);
+                    if (gmm) sts32(gam + 4u * (uint32_t)i, 0u);  // keep the gamma buffer all-zero
+                    const uint32_t a = gbase + state_off((uint32_t)i);
+                    const uint32_t f = lds32(a + NB), o = lds32(a + OB);
+                    sts32(a + NB, (f & ~M) | ((o ^ gmm) & M));
                 }
             }
             __syncthreads();
-            }
+        }
         if (wg == 0 && r > P.burn_in) {
             // A8: property indicator, bit-sliced over the group's chains
             uint32_t Iw = FULL;
             for (int k = 0; k < P.pred_k; ++k) {
-                const uint32_t w = lds32(bufB + 4u * P.pred_node[k]);
+                const uint32_t w = lds32(gbase + state_off(P.pred_node[k]) + NB);
                 Iw &= P.pred_val[k] ? w : ~w;
             }
             const uint32_t b = (Iw >> lane) & 1u;
@@ -600,19 +614,15 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         }
     };
     for (int64_t r = r_begin; r <= r_end; r += 2) {
-        step(r, bufA, bufB);
-        if (r + 1 <= r_end) step(r + 1, bufB, bufA);
+        step(r, std::integral_constant<uint32_t, 0u>());
+        if (r + 1 <= r_end) step(r + 1, std::integral_constant<uint32_t, 16u>());
     }
-    if (r_end >= r_begin && ((r_end - r_begin + 1) & 1)) {  // bufA holds the newest state
-        const uint32_t tmp = bufA;
-        bufA = bufB;
-        bufB = tmp;
-    }
+    if (r_end >= r_begin && ((r_end - r_begin + 1) & 1)) cur = 16u;  // odd step count: newest in buffer 1
 
     if (!last_chunk) {
         // suspend: bit-sliced state and warp-0 counters to scratch, then
         // release chunk c+1 of this group
-        for (int i = tid; i < n; i += blockDim.x) __stcg(scr + i, lds32(bufA + 4u * i));
+        for (int i = tid; i < n; i += blockDim.x) __stcg(scr + i, lds32(gbase + state_off(i) + cur));
         if (wg == 0) {
             uint32_t* st = scr + P.n_pad + 8 * lane;
             __stcg(st + 0, c1);
@@ -640,7 +650,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             for (int k = 0; k < 32; ++k) {
                 const int i = 32 * b + k;
                 if (i >= n) break;
-                v |= ((lds32(bufA + 4u * i) >> lane) & 1u) << k;
+                v |= ((lds32(gbase + state_off(i) + cur) >> lane) & 1u) << k;
             }
             if (valid) P.state[chain_local * nsw + b] = v;
         }
