@@ -235,6 +235,8 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
 
+    if args.sweep and args.config == "C4":
+        args.config = "C5"
     cfg = CONFIGS[args.config]
     args.chains = args.chains or cfg.chains
     args.burn_in = cfg.burn_in if args.burn_in is None else args.burn_in
@@ -246,12 +248,7 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.sweep:
-        if args.config == "C4":
-            args.config = "C5"
-        cfg = CONFIGS[args.config]
-        args.burn_in = cfg.burn_in if args.burn_in is None else args.burn_in
-        args.window = cfg.steps if args.window is None else args.window
-        run_sweep(args, cfg, config_model(args.config), config_predicate(args.config))
+        run_sweep(args, cfg, model, pred)
         return
     if args.impl == "reference":
         run_reference(args, cfg, model, pred, rank)

@@ -237,22 +237,31 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;
                 const int32_t theta = d->par_off[f + 1] - d->par_off[f];
-                // table padded to theta_max index bits: dummy parents are the low bits
-                uint64_t T = 0;
-                for (uint32_t idx = 0; idx < (1u << tm); ++idx)
-                    T |= (uint64_t)table_bit(d, f, idx >> (tm - theta)) << idx;
+                // table padded to FT index bits: dummy parents are the low bits
+                const uint32_t entries = 1u << tm;
+                std::vector<uint32_t> T((entries + 31) / 32, 0u);
+                for (uint32_t idx = 0; idx < entries; ++idx)
+                    T[idx >> 5] |= table_bit(d, f, idx >> (tm - theta)) << (idx & 31u);
                 uint32_t* w = B.u32(off_desc + ds * (uint32_t)j);
-                // stored bit-reversed per word: entry e at bit 31 - (e & 31)
-                int k = 0;
-                w[k++] = reverse_bits((uint32_t)T);
-                if (tm == 6) w[k++] = reverse_bits((uint32_t)(T >> 32));
-                // padded parent list, MSB first, as state-relative byte offsets;
-                // dummies read node 0
+                const uint32_t wbase = off_desc + ds * (uint32_t)j;
                 auto par = [&](int32_t m) { return pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u); };
-                for (int32_t m = 0; m < tm; ++m) {
-                    // relocated by the state base in shared memory (flag kRelocState)
-                    reloc.push_back((off_desc + ds * (uint32_t)j + 4u * (uint32_t)k) | pbn::kRelocState);
-                    w[k++] = par(m);
+                if (tm >= 7) {
+                    // {a[0..7] (a[7] padding when FT = 7), table words}
+                    for (int32_t m = 0; m < 8; ++m) {
+                        reloc.push_back((wbase + 4u * (uint32_t)m) | pbn::kRelocState);
+                        w[m] = par(m < tm ? m : tm);
+                    }
+                    // stored bit-reversed per word: entry e at bit 31 - (e & 31)
+                    for (size_t q = 0; q < T.size(); ++q) w[8 + q] = reverse_bits(T[q]);
+                } else {
+                    int k = 0;
+                    w[k++] = reverse_bits(T[0]);
+                    if (tm == 6) w[k++] = reverse_bits(T[1]);
+                    // padded parent list, MSB first, relocated by the state base
+                    for (int32_t m = 0; m < tm; ++m) {
+                        reloc.push_back((wbase + 4u * (uint32_t)k) | pbn::kRelocState);
+                        w[k++] = par(m);
+                    }
                 }
             }
             w3 = off_desc;

@@ -9,13 +9,15 @@
 //   nrec[i] (uint4, node i)       {E1, E2, E3, w}
 //       E_k  selection thresholds of reading Q3 as E_k = D_k - 1: the
 //            selected function is j = #{k : u > E_k}; unused = 0xFFFFFFFF
-//       w    FAST node (ell <= 4, theta_max <= 6): offset of the node's first
+//       w    FAST node (ell <= 4, theta_max <= 8): offset of the node's first
 //            fast descriptor (16-aligned, low 4 bits 0)
 //            SLOW node (anything else): offset of its slow record | 7
 //   fast descriptor (desc_bytes(FT) bytes, per function of a fast node,
-//            consecutive): u32 words {t0, [t1 if FT == 6], a[0..FT-1]}
+//            consecutive): u32 words {t0, [t1 if FT == 6], a[0..FT-1]} for
+//            FT <= 6; {a[0..7], 2^FT/32 table words} for FT = 7, 8 (the first
+//            FT-5 parents select the table word, loaded after the gather)
 //       every fast function is PADDED to the model-wide fast width FT (the
-//       largest theta over fast nodes, 3 <= FT <= 6): its parent list is
+//       largest theta over fast nodes, 3 <= FT <= 8): its parent list is
 //       extended with dummy parents that the table ignores
 //       (table'[idx'] = table[idx' >> (FT - theta)]), so every lane of a warp
 //       gathers exactly FT parents whatever function it chose -- straight-line
@@ -56,15 +58,21 @@
 namespace pbn {
 
 constexpr int kMaxPred = 16;
-constexpr int kMaxWarpsPerCta = 32;
+// threads per CTA the trajectory kernel is compiled for (register budget
+// 65536 / threads per thread); one 32-chain group's nodes are split over
+// these warps
+#ifndef PBN_MAX_THREADS
+#define PBN_MAX_THREADS 1024
+#endif
+constexpr int kMaxWarpsPerCta = PBN_MAX_THREADS / 32;
 constexpr uint32_t kSlowNode = 7;   // nrec.w low bits marking a slow node
 constexpr uint32_t kRelocState = 0x80000000u;  // relocation entry: add the state base
 // fast descriptor stride for fast width FT: t0 (+t1 when FT == 6) + FT offsets,
 // rounded up to 16 bytes
-__host__ __device__ constexpr uint32_t desc_bytes(int FT) { return FT == 3 ? 16u : 32u; }
+__host__ __device__ constexpr uint32_t desc_bytes(int FT) { return FT == 3 ? 16u : FT <= 6 ? 32u : FT == 7 ? 48u : 64u; }
 // byte offset of node i's word in buffer 0 of the group state
 __host__ __device__ constexpr uint32_t state_off(uint32_t i) { return 32u * (i >> 2) + 4u * (i & 3u); }
-constexpr int kFastMaxTheta = 6;
+constexpr int kFastMaxTheta = 8;
 constexpr int kFastMinTheta = 3;
 constexpr int kFastMaxEll = 4;
 

@@ -251,6 +251,7 @@ __device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w,
 template <uint32_t B>
 __device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t lmask)
 {
+    if (B == 0) return;
     asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
         "@p add.u32 %0, %0, %3;\n\t}"
         : "+r"(idx)
@@ -276,6 +277,29 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec
         if (u > rec.x) dp += DS;
         if (u > rec.y) dp += DS;
         if (u > rec.z) dp += DS;
+        // parent state word: absolute (relocated) address in shared-image
+        // launches, state-relative otherwise
+#define SB(x) (SMEM ? (x) : sb + (x))
+        uint32_t tw, idx = 0;
+        if constexpr (FT >= 7) {
+            // descriptor words {a[0..7], table words}: the first FT-5 parents
+            // pick one of the 2^(FT-5) table words (a dependent load), the other
+            // five index within it
+            const uint4 d0 = img.ld128(dp);
+            const uint4 d1 = img.ld128(dp + 16u);
+            const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+            constexpr int S = FT >= 7 ? FT - 5 : 2;
+            uint32_t widx = 0;
+            add_if_bit<(1u << (S - 1)) * 4u>(widx, lds32_state(SB(a[0]) + OB), lmask);
+            add_if_bit<(S > 1 ? 1u << (S - 2) : 0u) * 4u>(widx, lds32_state(SB(a[1]) + OB), lmask);
+            if (S > 2) add_if_bit<4u>(widx, lds32_state(SB(a[2 % FT]) + OB), lmask);
+            add_if_bit<16u>(idx, lds32_state(SB(a[S % 8]) + OB), lmask);
+            add_if_bit<8u>(idx, lds32_state(SB(a[(S + 1) % 8]) + OB), lmask);
+            add_if_bit<4u>(idx, lds32_state(SB(a[(S + 2) % 8]) + OB), lmask);
+            add_if_bit<2u>(idx, lds32_state(SB(a[(S + 3) % 8]) + OB), lmask);
+            add_if_bit<1u>(idx, lds32_state(SB(a[(S + 4) % 8]) + OB), lmask);
+            tw = img.ld32(dp + 32u + widx);
+        } else {
         // descriptor words {t0, [t1], a[0..FT-1]}: table word(s), then the FT
         // padded parents' state offsets, MSB first
         uint32_t tw0, tw1 = 0, a[6];
@@ -299,19 +323,16 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec
         // bit `lane` of its state word is set (LOP3 -> predicate, predicated add)
         // FT = 6: the first (most significant) parent picks the table word
         // (entries 32-63 in t1), the other five index within it
-        // parent state word: absolute (relocated) address in shared-image
-        // launches, state-relative otherwise
-#define SB(x) (SMEM ? (x) : sb + (x))
-        uint32_t tw = tw0;
+        tw = tw0;
         if (FT == 6) tw = (lds32_state(SB(a[0]) + OB) & lmask) ? tw1 : tw0;
         constexpr int S = FT == 6 ? 1 : 0;  // first parent handled above
         constexpr int R = FT - S;          // parents indexing within the word
-        uint32_t idx = 0;
         if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(SB(a[S + 0]) + OB), lmask);
         if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(SB(a[S + 1]) + OB), lmask);
         if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(SB(a[(S + 2) % 6]) + OB), lmask);
         if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(SB(a[(S + 3) % 6]) + OB), lmask);
         if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(SB(a[(S + 4) % 6]) + OB), lmask);
+        }
         // the table words are stored bit-REVERSED (entry e at bit 31 - (e & 31)),
         // so the entry is the sign bit of the word shifted left by idx
         bit = (uint32_t)((int32_t)(tw << idx) < 0);
@@ -329,7 +350,7 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec
 }
 
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
-__global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ TrajParams P)
+__global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_constant__ TrajParams P)
 {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -506,7 +527,7 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)
-        auto quad = [&](const int q, const uint4 rw) {
+        auto quad = [&](const int q, const uint4 rw, auto&& between) {
             const uint32_t i0 = 4u * (uint32_t)q;
             const uint32_t ra = nrec + 16u * i0;
             // the quad's four nodes are independent: compute all, then one
@@ -514,6 +535,9 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
             uint32_t g0, g1, g2, g3;
             const uint32_t w0 =
                 node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra, i0, rw.x, Tp, gbase, lmask, rot, g0);
+            // the next quad's Philox words, placed after the first vote so they
+            // share a basic block with (and interleave into) this quad's gathers
+            between();
             const uint32_t w1 =
                 node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 16u, i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
             const uint32_t w2 =
@@ -532,8 +556,8 @@ __global__ void __launch_bounds__(1024, 1) traj_kernel(const __grid_constant__ T
         // this quad's nodes gather (independent instruction streams)
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
         for (int q = q0; q < qf; ++q) {
-            const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
-            quad(q, rw);
+            uint4 rn;
+            quad(q, rw, [&] { rn = philox_quad((uint32_t)(q + 1), ps, P.rk); });
             rw = rn;
         }
         if (qf < q1) {  // ragged last quad (n % 4 != 0), node by node
@@ -706,7 +730,9 @@ const void* pick_ft(int FT, bool slow)
         case 3: return slow ? kptr<SMEM, PER_NODE, 3, true>() : kptr<SMEM, PER_NODE, 3, false>();
         case 4: return slow ? kptr<SMEM, PER_NODE, 4, true>() : kptr<SMEM, PER_NODE, 4, false>();
         case 5: return slow ? kptr<SMEM, PER_NODE, 5, true>() : kptr<SMEM, PER_NODE, 5, false>();
-        default: return slow ? kptr<SMEM, PER_NODE, 6, true>() : kptr<SMEM, PER_NODE, 6, false>();
+        case 6: return slow ? kptr<SMEM, PER_NODE, 6, true>() : kptr<SMEM, PER_NODE, 6, false>();
+        case 7: return slow ? kptr<SMEM, PER_NODE, 7, true>() : kptr<SMEM, PER_NODE, 7, false>();
+        default: return slow ? kptr<SMEM, PER_NODE, 8, true>() : kptr<SMEM, PER_NODE, 8, false>();
     }
 }
 

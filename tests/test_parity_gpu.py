@@ -155,6 +155,10 @@ def edge_models():
         np.array([0, 39], np.uint16), np.array([1, 1], np.uint8))
     yield "deep_theta_10", random_pbn(64, 1, 3, 6, 10, 0.002, seed=3), Predicate(
         np.array([1, 2, 3], np.uint16), np.array([0, 1, 0], np.uint8))
+    yield "theta_7_fast", random_pbn(48, 1, 4, 4, 7, 0.004, seed=6), Predicate(
+        np.array([5, 6], np.uint16), np.array([1, 0], np.uint8))
+    yield "theta_8_fast", random_pbn(61, 2, 4, 6, 8, 0.004, seed=7), Predicate(
+        np.array([60], np.uint16), np.array([1], np.uint8))
     yield "const_functions", random_pbn(37, 1, 4, 0, 1, 0.02, seed=4), Predicate(
         np.zeros(0, np.uint16), np.zeros(0, np.uint8))
     yield "heavy_perturbation", random_pbn(70, 1, 3, 1, 5, 0.3, seed=5), Predicate(
