@@ -263,12 +263,11 @@ __device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t 
 //   sb   state base (shared address of buffer-0 word of node 0; uniform)
 //   OB   byte offset of the OLD buffer (0 or 16, compile time)
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW, uint32_t OB>
-__device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec_addr, uint32_t i, uint32_t u,
+__device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, const uint4 rec, uint32_t i, uint32_t u,
                                               uint32_t Tp, uint32_t sb, uint32_t lmask, uint32_t rot,
                                               uint32_t& gw_out)
 {
     constexpr uint32_t DS = desc_bytes(FT);
-    const uint4 rec = img.ld128(rec_addr);
     const uint32_t gw = __ballot_sync(FULL, u < Tp);  // gamma_i(t) = 1 (A4)
     uint32_t bit;
     if (!SLOW || (rec.w & 7u) != kSlowNode) {
@@ -347,6 +346,19 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, uint32_t rec
     }
     gw_out = gw;
     return nb;
+}
+
+// node records {E1, E2, E3, w} of one quad
+struct Recs {
+    uint4 r[4];
+};
+template <bool SMEM>
+__device__ __forceinline__ Recs load_recs(const Img<SMEM>& img, uint32_t a)
+{
+    Recs x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x.r[k] = img.ld128(a + 16u * k);
+    return x;
 }
 
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
@@ -527,23 +539,22 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)
-        auto quad = [&](const int q, const uint4 rw, auto&& between) {
+        auto quad = [&](const int q, const uint4 rw, const Recs& rc, auto&& between) {
             const uint32_t i0 = 4u * (uint32_t)q;
-            const uint32_t ra = nrec + 16u * i0;
             // the quad's four nodes are independent: compute all, then one
             // 16-byte store commits them (and their gamma words if any)
             uint32_t g0, g1, g2, g3;
             const uint32_t w0 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra, i0, rw.x, Tp, gbase, lmask, rot, g0);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[0], i0, rw.x, Tp, gbase, lmask, rot, g0);
             // the next quad's Philox words, placed after the first vote so they
             // share a basic block with (and interleave into) this quad's gathers
             between();
             const uint32_t w1 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 16u, i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[1], i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
             const uint32_t w2 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 32u, i0 + 2, rw.z, Tp, gbase, lmask, rot, g2);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[2], i0 + 2, rw.z, Tp, gbase, lmask, rot, g2);
             const uint32_t w3 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 48u, i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[3], i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
             sts128_if(gbase + 32u * (uint32_t)q + NB, w0, w1, w2, w3, lead);
             if (!PER_NODE) {
                 const uint32_t g = g0 | g1 | g2 | g3;
@@ -555,11 +566,26 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         // software pipeline: the next quad's Philox words are computed while
         // this quad's nodes gather (independent instruction streams)
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
+#ifdef PBN_PREFETCH_REC
+        // the next quad's node records are loaded with its Philox words
+        Recs rc = load_recs(img, nrec + 64u * (uint32_t)q0);
         for (int q = q0; q < qf; ++q) {
             uint4 rn;
-            quad(q, rw, [&] { rn = philox_quad((uint32_t)(q + 1), ps, P.rk); });
+            Recs rcn;
+            quad(q, rw, rc, [&] {
+                rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
+                rcn = load_recs(img, nrec + 64u * (uint32_t)(q + 1 < qf ? q + 1 : q));
+            });
+            rw = rn;
+            rc = rcn;
+        }
+#else
+        for (int q = q0; q < qf; ++q) {
+            uint4 rn;
+            quad(q, rw, load_recs(img, nrec + 64u * (uint32_t)q), [&] { rn = philox_quad((uint32_t)(q + 1), ps, P.rk); });
             rw = rn;
         }
+#endif
         if (qf < q1) {  // ragged last quad (n % 4 != 0), node by node
             const int q = qf;
             const uint32_t i0 = 4u * (uint32_t)q;
@@ -567,7 +593,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             const uint32_t rr[4] = {rw.x, rw.y, rw.z, rw.w};
             for (uint32_t k = 0; k < 4 && (int)(i0 + k) < n; ++k) {
                 uint32_t gk;
-                const uint32_t wk = node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, ra + 16u * k, i0 + k, rr[k], Tp,
+                const uint32_t wk = node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, img.ld128(ra + 16u * k), i0 + k, rr[k], Tp,
                                                                             gbase, lmask, rot, gk);
                 sts32_if(gbase + 32u * (uint32_t)q + NB + 4u * k, wk, lead);
                 if (!PER_NODE) {
