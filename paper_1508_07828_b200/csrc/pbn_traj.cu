@@ -546,15 +546,15 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             uint32_t g0, g1, g2, g3;
             const uint32_t w0 =
                 node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[0], i0, rw.x, Tp, gbase, lmask, rot, g0);
-            // the next quad's Philox words, placed after the first vote so they
-            // share a basic block with (and interleave into) this quad's gathers
-            between();
             const uint32_t w1 =
                 node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[1], i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
             const uint32_t w2 =
                 node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[2], i0 + 2, rw.z, Tp, gbase, lmask, rot, g2);
             const uint32_t w3 =
                 node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[3], i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
+            // the next quad's Philox words: after the votes, in the same basic
+            // block as (and interleaved by the scheduler into) this quad's gathers
+            between();
             sts128_if(gbase + 32u * (uint32_t)q + NB, w0, w1, w2, w3, lead);
             if (!PER_NODE) {
                 const uint32_t g = g0 | g1 | g2 | g3;
