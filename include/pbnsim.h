@@ -75,10 +75,11 @@ typedef struct {
     uint32_t flags;
 } pbn_model_desc;
 
-#define PBN_MAX_NODES 16383   /* parent addresses are 16-bit byte offsets      */
+#define PBN_MAX_NODES 16383   /* one group's state must fit in shared memory   */
 #define PBN_MAX_THETA 16      /* parents per predictor function                */
 #define PBN_MAX_ELL   128     /* predictor functions per node                  */
 #define PBN_MAX_PRED  16      /* (node, value) pairs in a property             */
+#define PBN_MAX_PROPS 8       /* properties evaluated by one pbn_simulate call */
 
 /* Host-only validation: returns PBN_OK or PBN_E_INVALID with a
  * message naming the node and the violated rule.  Needs no GPU. */
@@ -142,6 +143,10 @@ typedef struct {
  *                (group, chunk of chunk_steps steps) units, state carried
  *                between chunks in a stream-ordered scratch allocation
  *   chunk_steps  persistent chunk length (0 = auto)
+ *   n_props, props  several properties from the same trajectories (the
+ *                multi-property reuse of P:507-526): every statistic below is
+ *                produced per property, property-major (property p's block
+ *                follows property p-1's; block sizes as for one property)
  * The launch-shape fields never change any output. */
 typedef struct {
     int64_t n_chains;
@@ -160,6 +165,8 @@ typedef struct {
     int32_t warps_per_group;
     int32_t schedule;
     int64_t chunk_steps;
+    int32_t n_props;                /* 0: one property, `pred`; 1..PBN_MAX_PROPS:  */
+    const pbn_predicate* props;     /*    props[0..n_props-1] (pred ignored)       */
 } pbn_sim_args;
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).
@@ -175,7 +182,10 @@ typedef struct {
  *   totals      [6] u64, overwritten: S1 = sum c1, S2 = sum c1^2, sum n01,
  *               sum n10, sum n0from, sum n1from, where n0from / n1from count
  *               window elements with a successor that are 0 / 1 (A10).
- * Any pointer except state may be NULL if not wanted (totals NULL skips A10). */
+ * Any pointer except state may be NULL if not wanted (totals NULL skips A10).
+ * With n_props = q > 1 every array except state holds q property-major
+ * blocks: c1[p*n_chains + c], bits[(p*n_chains + c)*bits_row_words + w],
+ * batch_sums[(p*n_chains + c)*ceil(steps/batch) + b], totals[6*p + k]. */
 typedef struct {
     uint32_t* state;
     uint32_t* c1;
@@ -283,6 +293,32 @@ typedef struct {
 
 pbn_status pbn_run(pbn_model model, const pbn_run_args* args, pbn_run_result* res,
                    void* cuda_stream, char* err, size_t errlen);
+
+/* Several properties from one set of trajectories: Algorithm 3, then
+ * Algorithm 4 with the multi-property reuse of samples (reading
+ * Q13).  The omega chains are abstracted into n_props meta-state sequences
+ * in the same kernel launches (pbn_simulate with n_props).  Gelman & Rubin
+ * converges when every property with non-constant windows has R-hat below
+ * the threshold; the pooled sample then grows to the smallest per-property
+ * N that is not yet met until every N is met; the burn-in
+ * re-check uses the largest M.  args->method must be PBN_METHOD_TWO_STATE;
+ * args->pred is ignored.  per_prop[n_props] receives each property's
+ * estimate, M, N, alpha, beta, R-hat and status (PBN_E_DEGENERATE for a
+ * property whose two-state statistics are undefined: it is reported, not
+ * fatal, and does not drive the extension).  res receives the shared
+ * numbers (psi, pooled sample size, steps per chain, iterations, largest
+ * R-hat; estimate/M/N/alpha/beta of property 0). */
+typedef struct {
+    double estimate;
+    double rhat;
+    double alpha, beta;
+    int64_t M, N;
+    int32_t status;          /* pbn_status of this property's two-state step  */
+} pbn_prop_result;
+
+pbn_status pbn_run_multi(pbn_model model, const pbn_run_args* args, const pbn_predicate* props,
+                         int32_t n_props, pbn_run_result* res, pbn_prop_result* per_prop,
+                         void* cuda_stream, char* err, size_t errlen);
 
 /* Version string of the build, e.g. "libpbnsim 0.1 sm_100a". */
 const char* pbn_version(void);

@@ -23,6 +23,7 @@ from .api import (  # noqa: F401
     pbn_t_quantile,
     pbn_skart_ci_from_batches,
     pbn_run,
+    pbn_run_multi,
     pbn_version,
     alloc_outputs,
     PbnError,

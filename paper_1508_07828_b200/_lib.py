@@ -64,7 +64,8 @@ class pbn_sim_args(C.Structure):
                 ("seed", C.c_uint64), ("pred", pbn_predicate), ("init", C.c_int32),
                 ("emit_bits", C.c_int32), ("bits_offset", C.c_int64), ("bits_row_words", C.c_int64),
                 ("groups_per_cta", C.c_int32), ("warps_per_group", C.c_int32),
-                ("schedule", C.c_int32), ("chunk_steps", C.c_int64)]
+                ("schedule", C.c_int32), ("chunk_steps", C.c_int64), ("n_props", C.c_int32),
+                ("props", C.c_void_p)]
 
 
 class pbn_sim_out(C.Structure):
@@ -88,6 +89,11 @@ class pbn_run_args(C.Structure):
                 ("rhat_threshold", C.c_double), ("r", C.c_double), ("s", C.c_double),
                 ("eps", C.c_double), ("h_star", C.c_double), ("alpha_conf", C.c_double),
                 ("seed", C.c_uint64), ("pred", pbn_predicate), ("max_steps", C.c_int64)]
+
+
+class pbn_prop_result(C.Structure):
+    _fields_ = [("estimate", C.c_double), ("rhat", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
+                ("M", C.c_int64), ("N", C.c_int64), ("status", C.c_int32)]
 
 
 class pbn_run_result(C.Structure):
@@ -120,6 +126,8 @@ SIGNATURES = {
                                             C.POINTER(pbn_skart_ci)]),
     "pbn_run": (C.c_int, [C.c_void_p, C.POINTER(pbn_run_args), C.POINTER(pbn_run_result), C.c_void_p,
                           C.c_char_p, C.c_size_t]),
+    "pbn_run_multi": (C.c_int, [C.c_void_p, C.POINTER(pbn_run_args), C.c_void_p, C.c_int32,
+                                C.POINTER(pbn_run_result), C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t]),
     "pbn_version": (C.c_char_p, []),
 }
 

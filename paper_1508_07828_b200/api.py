@@ -110,23 +110,26 @@ class SimOutputs:
 
 
 def alloc_outputs(model: Model, n_chains: int, steps: int, batch: int = 0, emit_bits: bool = False,
-                  bits_row_words: int = 0, device="cuda") -> SimOutputs:
+                  bits_row_words: int = 0, device="cuda", n_props: int = 0) -> SimOutputs:
+    """Device buffers for pbn_simulate.  n_props = q >= 1 gives q
+    property-major blocks (leading dimension q) for every output but state."""
     import torch
     dev = torch.device(device)
     i32 = torch.int32
+    lead = (n_props,) if n_props > 0 else ()
     out = SimOutputs(
         state=torch.zeros((n_chains, model.state_words), dtype=i32, device=dev),
-        c1=torch.empty(n_chains, dtype=i32, device=dev),
-        n01=torch.empty(n_chains, dtype=i32, device=dev),
-        n10=torch.empty(n_chains, dtype=i32, device=dev),
-        first_last=torch.empty(n_chains, dtype=torch.uint8, device=dev),
-        totals=torch.zeros(6, dtype=torch.int64, device=dev),
+        c1=torch.empty(lead + (n_chains,), dtype=i32, device=dev),
+        n01=torch.empty(lead + (n_chains,), dtype=i32, device=dev),
+        n10=torch.empty(lead + (n_chains,), dtype=i32, device=dev),
+        first_last=torch.empty(lead + (n_chains,), dtype=torch.uint8, device=dev),
+        totals=torch.zeros(lead + (6,), dtype=torch.int64, device=dev),
     )
     if batch > 0:
-        out.batch_sums = torch.empty((n_chains, (steps + batch - 1) // batch), dtype=i32, device=dev)
+        out.batch_sums = torch.empty(lead + (n_chains, (steps + batch - 1) // batch), dtype=i32, device=dev)
     if emit_bits:
         rw = bits_row_words or (steps + 31) // 32
-        out.bits = torch.zeros((n_chains, rw), dtype=i32, device=dev)
+        out.bits = torch.zeros(lead + (n_chains, rw), dtype=i32, device=dev)
     return out
 
 
@@ -151,15 +154,26 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                  step0: int = 0, burn_in: int = 0, batch: int = 0, seed: int = 0, pred=None,
                  init: bool = False, emit_bits: bool = False, bits_offset: int = 0,
                  bits_row_words: int = 0, groups_per_cta: int = 0, warps_per_group: int = 0,
-                 schedule: int = 0, chunk_steps: int = 0, stream=None) -> None:
+                 schedule: int = 0, chunk_steps: int = 0, stream=None, props=None) -> None:
+    """props: a list of q >= 1 predicates evaluated on the same trajectories
+    (multi-property reuse); `pred` is then ignored."""
     cp, _keep = _pred(pred)
+    keep_props = None
+    n_props, props_ptr = 0, None
+    if props:
+        items = [_pred(p) for p in props]
+        arr = (L.pbn_predicate * len(items))(*[it[0] for it in items])
+        keep_props = (arr, [it[1] for it in items])
+        n_props, props_ptr = len(items), C.cast(arr, C.c_void_p)
     a = L.pbn_sim_args(n_chains=n_chains, chain_base=chain_base, step0=step0, burn_in=burn_in,
                        steps=steps, batch=batch, seed=seed, pred=cp, init=int(bool(init)),
                        emit_bits=int(bool(emit_bits)), bits_offset=bits_offset,
                        bits_row_words=bits_row_words, groups_per_cta=groups_per_cta,
-                       warps_per_group=warps_per_group, schedule=schedule, chunk_steps=chunk_steps)
+                       warps_per_group=warps_per_group, schedule=schedule, chunk_steps=chunk_steps,
+                       n_props=n_props, props=props_ptr)
     o = out.c_struct()
     check(lib().pbn_simulate(model.handle, C.byref(a), C.byref(o), _stream_handle(stream)))
+    del keep_props  # the predicate arrays are read synchronously by the call above
 
 
 def pbn_recount(bits, n_chains: int, row_words: int, start: int, length: int, batch: int = 0,
@@ -216,3 +230,21 @@ def pbn_run(model: Model, *, method: int = 0, omega: int, psi0: int, rhat_thresh
     err = C.create_string_buffer(512)
     st = lib().pbn_run(model.handle, C.byref(a), C.byref(res), _stream_handle(stream), err, 512)
     return st, res, err.value.decode(errors="replace")
+
+
+def pbn_run_multi(model: Model, props, *, omega: int, psi0: int, rhat_threshold: float = 1.1,
+                  r: float = 0.01, s: float = 0.95, eps: float = 1e-10, seed: int = 0,
+                  max_steps: int = 1 << 26, stream=None):
+    """Algorithm 3 + Algorithm 4 for several properties on shared samples
+    (P:507-526).  Returns (status, run_result, [per-property results], err)."""
+    items = [_pred(p) for p in props]
+    arr = (L.pbn_predicate * len(items))(*[it[0] for it in items])
+    a = L.pbn_run_args(method=0, omega=omega, psi0=psi0, rhat_threshold=rhat_threshold, r=r, s=s,
+                       eps=eps, seed=seed, max_steps=max_steps)
+    res = L.pbn_run_result()
+    per = (L.pbn_prop_result * len(items))()
+    err = C.create_string_buffer(512)
+    st = lib().pbn_run_multi(model.handle, C.byref(a), C.cast(arr, C.c_void_p), len(items), C.byref(res),
+                             C.cast(per, C.c_void_p), _stream_handle(stream), err, 512)
+    del items
+    return st, res, list(per), err.value.decode(errors="replace")

@@ -404,8 +404,13 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     if (a->chain_base + a->n_chains > (int64_t)kTwo32) return PBN_E_USAGE;
     if (a->steps >= (int64_t)kTwo32) return PBN_E_USAGE;  // u32 counters
     if (a->init && a->step0 != 0) return PBN_E_USAGE;
-    if (a->pred.k < 0 || a->pred.k > PBN_MAX_PRED) return PBN_E_USAGE;
-    if (a->pred.k > 0 && (!a->pred.node || !a->pred.value)) return PBN_E_USAGE;
+    if (a->n_props < 0 || a->n_props > PBN_MAX_PROPS || (a->n_props > 0 && !a->props)) return PBN_E_USAGE;
+    const int nprops = a->n_props > 0 ? a->n_props : 1;
+    const pbn_predicate* props = a->n_props > 0 ? a->props : &a->pred;
+    for (int p = 0; p < nprops; ++p) {
+        if (props[p].k < 0 || props[p].k > PBN_MAX_PRED) return PBN_E_USAGE;
+        if (props[p].k > 0 && (!props[p].node || !props[p].value)) return PBN_E_USAGE;
+    }
     if (a->steps > 0 && a->batch > 0 && !o->batch_sums) return PBN_E_USAGE;
     if (a->steps > 0 && a->emit_bits && !o->bits) return PBN_E_USAGE;
     if (a->bits_offset < 0 || a->bits_row_words < 0) return PBN_E_USAGE;
@@ -434,11 +439,14 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     P->batch = a->batch;
     P->init = a->init ? 1 : 0;
     P->emit_bits = a->emit_bits ? 1 : 0;
-    P->pred_k = a->pred.k;
-    for (int k = 0; k < a->pred.k; ++k) {
-        if ((int32_t)a->pred.node[k] >= m->L.n || a->pred.value[k] > 1) return PBN_E_INVALID;
-        P->pred_node[k] = a->pred.node[k];
-        P->pred_val[k] = a->pred.value[k];
+    P->n_props = nprops;
+    for (int p = 0; p < nprops; ++p) {
+        P->pred_k[p] = props[p].k;
+        for (int k = 0; k < props[p].k; ++k) {
+            if ((int32_t)props[p].node[k] >= m->L.n || props[p].value[k] > 1) return PBN_E_INVALID;
+            P->pred_node[p][k] = props[p].node[k];
+            P->pred_val[p][k] = props[p].value[k];
+        }
     }
     P->batch_row = a->batch > 0 ? (a->steps + a->batch - 1) / a->batch : 0;
     const int64_t need_words = (a->bits_offset + a->steps + 31) / 32;
@@ -463,7 +471,8 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     if (st != PBN_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     if (o->totals) {
-        if (cudaMemsetAsync(o->totals, 0, 6 * sizeof(uint64_t), s) != cudaSuccess) return PBN_E_CUDA;
+        if (cudaMemsetAsync(o->totals, 0, 6 * sizeof(uint64_t) * (size_t)P.n_props, s) != cudaSuccess)
+            return PBN_E_CUDA;
     }
     if (a->n_chains == 0) return PBN_OK;
     pbn::LaunchPlan plan;

@@ -58,6 +58,7 @@
 namespace pbn {
 
 constexpr int kMaxPred = 16;
+constexpr int kMaxProps = 8;   // properties per launch (multi-property reuse)
 // threads per CTA the trajectory kernel is compiled for (register budget
 // 65536 / threads per thread); one 32-chain group's nodes are split over
 // these warps
@@ -101,9 +102,12 @@ struct TrajParams {
     uint32_t image_smem_bytes; // 0 when the image is read from global memory
     int64_t n_chains, chain_base, step0, burn_in, steps, batch;
     int32_t init, emit_bits;
-    int32_t pred_k;
-    uint16_t pred_node[kMaxPred];
-    uint8_t pred_val[kMaxPred];
+    // properties: warp p < n_props evaluates property p and keeps its
+    // per-chain statistics (outputs property-major, stride n_chains)
+    int32_t n_props;
+    int32_t pred_k[kMaxProps];
+    uint16_t pred_node[kMaxProps][kMaxPred];
+    uint8_t pred_val[kMaxProps][kMaxPred];
     // persistent scheduling (grid = resident CTAs; units = (group, step chunk))
     int32_t persistent;
     int64_t n_groups;          // ceil(n_chains / 32)
@@ -112,7 +116,7 @@ struct TrajParams {
     unsigned long long* work_ctr;  // unit queue head (zeroed per launch)
     uint32_t* done;            // [n_groups] chunks completed per group (zeroed per launch)
     uint32_t* scratch;         // [n_groups x scratch_stride] suspended group state
-    int64_t scratch_stride;    // n_pad + 8 * 32 words
+    int64_t scratch_stride;    // n_pad + 8 * 32 * n_props words
     int64_t batch_row;         // ceil(steps/batch) (0 if no batches)
     int64_t bits_row;          // row stride of bits in u32
     int64_t bits_offset;       // window element w -> row bit bits_offset + w
@@ -124,7 +128,7 @@ struct TrajParams {
     uint8_t* first_last;
     uint32_t* batch_sums;
     uint32_t* bits;
-    unsigned long long* totals;
+    unsigned long long* totals;  // [6 x n_props]
 };
 
 struct LaunchPlan {

@@ -480,6 +480,10 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         // chunk starts from buffer 0, `cur` tracks the newest buffer
         uint32_t cur = 0;
         uint32_t* scr = P.scratch + group * (int64_t)P.scratch_stride;  // persistent only
+        // statistics warp: warp p < n_props owns property p (A8-A10)
+        const int prop = wg;
+        const bool stats = prop < P.n_props;
+        const int64_t pofs = (int64_t)prop * P.n_chains;  // property-major outputs
 
         // ---- per-lane statistics (warp 0) ----
         uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0, bcount = 0;
@@ -488,8 +492,8 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             // resume: bit-sliced state words and warp-0 counters from scratch
             __syncthreads();
             for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr + i));
-            if (wg == 0) {
-                const uint32_t* st = scr + P.n_pad + 8 * lane;
+            if (stats) {
+                const uint32_t* st = scr + P.n_pad + 8 * 32 * prop + 8 * lane;
                 c1 = __ldcg(st + 0);
                 n01 = __ldcg(st + 1);
                 n10 = __ldcg(st + 2);
@@ -619,12 +623,12 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             }
             __syncthreads();
         }
-        if (wg == 0 && r > P.burn_in) {
+        if (stats && r > P.burn_in) {
             // A8: property indicator, bit-sliced over the group's chains
             uint32_t Iw = FULL;
-            for (int k = 0; k < P.pred_k; ++k) {
-                const uint32_t w = lds32(gbase + state_off(P.pred_node[k]) + NB);
-                Iw &= P.pred_val[k] ? w : ~w;
+            for (int k = 0; k < P.pred_k[prop]; ++k) {
+                const uint32_t w = lds32(gbase + state_off(P.pred_node[prop][k]) + NB);
+                Iw &= P.pred_val[prop][k] ? w : ~w;
             }
             const uint32_t b = (Iw >> lane) & 1u;
             const int64_t wpos = r - P.burn_in - 1;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             if (P.batch > 0) {
                 bacc += b;
                 if (++bcount == P.batch || wpos + 1 == P.steps) {
-                    if (valid) P.batch_sums[chain_local * P.batch_row + wpos / P.batch] = bacc;
+                    if (valid) P.batch_sums[(pofs + chain_local) * P.batch_row + wpos / P.batch] = bacc;
                     bacc = 0;
                     bcount = 0;
                 }
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
                 const bool word_end = (bpos & 31) == 31;
                 if (word_end || wpos + 1 == P.steps) {
                     if (valid) {
-                        uint32_t* dst = P.bits + chain_local * P.bits_row + (bpos >> 5);
+                        uint32_t* dst = P.bits + (pofs + chain_local) * P.bits_row + (bpos >> 5);
                         // the word holding bit bits_offset keeps its lower (earlier)
                         // bits: OR-merge; every other word is overwritten
                         const bool own = (bpos & ~(int64_t)31) >= P.bits_offset;
@@ -673,8 +677,8 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         // suspend: bit-sliced state and warp-0 counters to scratch, then
         // release chunk c+1 of this group
         for (int i = tid; i < n; i += blockDim.x) __stcg(scr + i, lds32(gbase + state_off(i) + cur));
-        if (wg == 0) {
-            uint32_t* st = scr + P.n_pad + 8 * lane;
+        if (stats) {
+            uint32_t* st = scr + P.n_pad + 8 * 32 * prop + 8 * lane;
             __stcg(st + 0, c1);
             __stcg(st + 1, n01);
             __stcg(st + 2, n10);
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             if (valid) P.state[chain_local * nsw + b] = v;
         }
     }
-    if (wg == 0) {
+    if (stats) {
         const uint32_t last = prev;
         const int64_t Wn = P.steps;
         uint32_t n0from = 0, n1from = 0;
@@ -714,10 +718,10 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             n0from = (uint32_t)(Wn - c1) - (1u - last);
         }
         if (valid) {
-            if (P.c1) P.c1[chain_local] = c1;
-            if (P.n01) P.n01[chain_local] = n01;
-            if (P.n10) P.n10[chain_local] = n10;
-            if (P.first_last) P.first_last[chain_local] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
+            if (P.c1) P.c1[pofs + chain_local] = c1;
+            if (P.n01) P.n01[pofs + chain_local] = n01;
+            if (P.n10) P.n10[pofs + chain_local] = n10;
+            if (P.first_last) P.first_last[pofs + chain_local] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
         }
         if (P.totals) {
             unsigned long long v[6];
@@ -735,7 +739,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             if (leader) {
 #pragma unroll
                 for (int k = 0; k < 6; ++k)
-                    if (v[k]) atomicAdd(P.totals + k, v[k]);
+                    if (v[k]) atomicAdd(P.totals + 6 * prop + k, v[k]);
             }
         }
     }
@@ -791,9 +795,11 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
         *why = "network too large: one 32-chain group's state does not fit in shared memory";
         return -1;
     }
+    // every property needs a statistics warp: at least n_props warps
     int Wp = want_warps > 0 ? want_warps : std::max(1, std::min(kMaxWarpsPerCta, P.nquads));
-    if (Wp > kMaxWarpsPerCta || Wp > P.nquads) {
-        *why = "warps_per_group must be <= 32 and <= ceil(n/4)";
+    Wp = std::max(Wp, P.n_props);
+    if (Wp > kMaxWarpsPerCta || Wp > std::max(P.nquads, P.n_props)) {
+        *why = "warps_per_group must be <= the CTA warp budget and <= max(ceil(n/4), properties)";
         return -1;
     }
     plan->warps_per_group = Wp;
@@ -840,7 +846,7 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
         P.n_groups = G;
         P.chunk_steps = K;
         P.total_units = G * ((total + K - 1) / K);
-        P.scratch_stride = P.n_pad + 8 * 32;
+        P.scratch_stride = P.n_pad + 8 * 32 * (int64_t)std::max(P.n_props, 1);
         const size_t scratch_bytes = (size_t)G * (size_t)P.scratch_stride * 4;
         const size_t ctl_bytes = 8 + (size_t)G * 4;
         e = cudaMallocAsync(reinterpret_cast<void**>(&ws), scratch_bytes + ctl_bytes + 16, s);

@@ -38,12 +38,13 @@ def sample_chain_ids(n_chains: int, k: int = 8, seed: int = 0) -> list[int]:
 
 def gpu_run(pm, model, pred, *, n_chains, steps, burn_in=0, step0=0, chain_base=0, seed=1, batch=0,
             emit_bits=True, init=True, state=None, groups=0, warps=0, bits_offset=0,
-            bits_row_words=0, bits_init=None, schedule=0, chunk_steps=0):
-    """Run pbn_simulate; returns a dict of host numpy arrays."""
+            bits_row_words=0, bits_init=None, schedule=0, chunk_steps=0, props=None):
+    """Run pbn_simulate; returns a dict of host numpy arrays (with `props`,
+    every field but state has a leading property dimension)."""
     import torch
     import paper_1508_07828_b200 as pbn
     out = pbn.alloc_outputs(pm, n_chains, steps, batch=batch, emit_bits=emit_bits,
-                            bits_row_words=bits_row_words)
+                            bits_row_words=bits_row_words, n_props=len(props) if props else 0)
     if state is not None:
         out.state.copy_(torch.from_numpy(np.ascontiguousarray(state).view(np.int32)).cuda())
     if bits_init is not None:
@@ -52,7 +53,7 @@ def gpu_run(pm, model, pred, *, n_chains, steps, burn_in=0, step0=0, chain_base=
                      burn_in=burn_in, batch=batch, seed=seed, pred=pred, init=init,
                      emit_bits=emit_bits, bits_offset=bits_offset, bits_row_words=bits_row_words,
                      groups_per_cta=groups, warps_per_group=warps, schedule=schedule,
-                     chunk_steps=chunk_steps)
+                     chunk_steps=chunk_steps, props=props)
     torch.cuda.synchronize()
 
     def h(t):

@@ -214,3 +214,43 @@ def test_recount_matches_oracle_subwindows(pbn):
         if batch:
             assert np.array_equal(bs.cpu().numpy()[:, :nb], np.stack([w.batch_sums for w in ws]))
         assert np.array_equal(tot.cpu().numpy().view(np.uint64), ostats.totals(ws))
+
+
+def random_props(model, q, rng, kmax=4):
+    out = []
+    for _ in range(q):
+        k = int(rng.integers(0, kmax + 1))
+        nodes = rng.choice(model.n, size=k, replace=False).astype(np.uint16)
+        out.append(Predicate(nodes, rng.integers(0, 2, size=k).astype(np.uint8)))
+    return out
+
+
+FIELDS = ["c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]
+
+
+@pytest.mark.parametrize("key,q,chains,steps,burn_in,schedule", [
+    ("C1", 8, 45, 700, 100, 0),      # n = 10: 3 quads, 8 statistics warps
+    ("C2", 5, 200, 600, 150, 0),
+    ("C2", 3, 20000, 120, 40, 2),    # persistent chunks carry every property's counters
+])
+def test_multi_property_equals_single_property_runs(pbn, key, q, chains, steps, burn_in, schedule):
+    """q properties abstracted from the same trajectories in one
+    launch give exactly the q single-property results."""
+    model = config_model(key)
+    rng = np.random.default_rng(q)
+    props = random_props(model, q, rng)
+    pm = load(pbn, model)
+    m = gpu_run(pm, model, None, n_chains=chains, steps=steps, burn_in=burn_in, seed=11, batch=64,
+                props=props, schedule=schedule, chunk_steps=37 if schedule == 2 else 0)
+    for p, pr in enumerate(props):
+        s = gpu_run(pm, model, pr, n_chains=chains, steps=steps, burn_in=burn_in, seed=11, batch=64)
+        assert np.array_equal(m["state"], s["state"])
+        for k in FIELDS:
+            assert np.array_equal(m[k][p], s[k]), (p, k)
+    # and one property against the oracle on a few chains
+    ids = sample_chain_ids(chains, k=4, seed=q)
+    st, I, ws = oracle_run(model, props[-1], ids, steps=steps, burn_in=burn_in, seed=11, batch=64)
+    packed = pack_states(st)
+    last = {k: (m[k][q - 1] if k != "state" else m[k]) for k in ["state"] + FIELDS}
+    for j, cid in enumerate(ids):
+        compare_chain(last, cid, packed[j], ws[j], steps, 64)
