@@ -121,6 +121,97 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
 
 
 # --------------------------------------------------------------------------
+# Algorithm 4 with the multi-property reuse of samples (reading Q13)
+# --------------------------------------------------------------------------
+@dataclass
+class MultiResult:
+    rhat: float
+    psi: int
+    steps_per_chain: int
+    gr_iterations: int
+    extensions: int
+    sample_size: int
+    per_prop: list          # per property: dict(estimate, M, N, alpha, beta, degenerate)
+
+
+def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, threshold: float, r: float,
+                             s: float, eps: float, max_steps: int, threads: int = 8) -> MultiResult:
+    """q properties checked on one set of omega trajectories.
+
+    "The simulated samples are abstracted into different meta states based on
+    these different q properties simultaneously": one oracle
+    chain set per property, all with the same seed and chain ids, hence the
+    same trajectories.  Gelman & Rubin: converged when every property with
+    non-constant windows has R-hat < threshold (Q8).  "The next extension
+    length is determined by the minimal value of all the calculated Ns"
+    (P:521): grow the pooled sample to the smallest N_p not yet met, then
+    re-evaluate; stop "when all the calculated Ns are smaller than the
+    current sample size".  Degenerate properties are reported and do
+    not drive the extension.  Burn-in re-check with the largest
+    M_p (reading Q9)."""
+    q = len(preds)
+    chs = [Chains(model, pr, seed, omega, threads) for pr in preds]
+    psi = psi0
+    windows = [ch.advance(psi, psi) for ch in chs]
+    it = 0
+    while True:
+        it += 1
+        rh = []
+        for w in windows:
+            if np.any(w.var(axis=1) > 0):
+                rh.append(ost.gelman_rubin_windows(w).rhat)
+        if rh and all(x < threshold for x in rh):
+            rhat = max(rh)
+            break
+        if 4 * psi > max_steps:
+            raise RuntimeError("Gelman-Rubin did not converge within the step cap")
+        psi *= 2
+        windows = [ch.advance(0, psi) for ch in chs]
+    seqs = [[[int(v) for v in w[c]] for c in range(omega)] for w in windows]
+    disc, ext_count = 0, 0
+    while True:
+        while True:
+            L = len(seqs[0][0]) - disc
+            ts = []
+            for p in range(q):
+                counts = ost.estimate_alpha_beta([np.asarray(x[disc:]) for x in seqs[p]]) if L >= 2 else None
+                t = ost.two_state(*counts, r, s, eps) if counts is not None else None
+                ts.append(t if (t is not None and not t.degenerate) else None)
+            usable = [t for t in ts if t is not None]
+            if usable:
+                unmet = [t.N for t in usable if t.N > omega * L]
+                if not unmet:
+                    break
+                ext = -(-(min(unmet) - omega * L) // omega)
+            else:
+                ext = max(L, psi)
+            if chs[0].length + ext > max_steps:
+                raise RuntimeError("two-state sample exceeds the step cap")
+            for p in range(q):
+                I = chs[p].advance(0, ext)
+                for c in range(omega):
+                    seqs[p][c].extend(int(v) for v in I[c])
+            ext_count += 1
+        Mmax = max([t.M for t in ts if t is not None], default=0)
+        if Mmax > psi:
+            disc += Mmax - psi
+            psi = Mmax
+            disc = min(disc, len(seqs[0][0]))
+            continue
+        break
+    L = len(seqs[0][0]) - disc
+    per = []
+    for p in range(q):
+        ones = sum(sum(x[disc:]) for x in seqs[p])
+        t = ts[p]
+        per.append({"estimate": ones / (omega * L), "degenerate": t is None,
+                    "M": t.M if t else 0, "N": t.N if t else 0,
+                    "alpha": t.alpha if t else float("nan"), "beta": t.beta if t else float("nan")})
+    return MultiResult(rhat=rhat, psi=psi, steps_per_chain=chs[0].length, gr_iterations=it,
+                       extensions=ext_count, sample_size=omega * L, per_prop=per)
+
+
+# --------------------------------------------------------------------------
 # Algorithm 5 (parallel Skart), constants of SPEC S:375 (reading Q11/Q12)
 # --------------------------------------------------------------------------
 SKEW_LIMIT = 4.0          # |B| <= 4 -> kappa = 1, else 16

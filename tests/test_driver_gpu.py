@@ -91,3 +91,39 @@ def test_skart_driver(pbn, omega, seed):
     for a, b in [(res.estimate, o.estimate), (res.ci_lo, o.ci_lo), (res.ci_hi, o.ci_hi), (res.rhat, o.rhat)]:
         assert close(a, b), (a, b)
     assert res.ci_lo <= res.estimate <= res.ci_hi
+
+
+def _multi_props(model, q, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(q):
+        k = int(rng.integers(1, 3))
+        nodes = rng.choice(model.n, size=k, replace=False).astype(np.uint16)
+        out.append(Predicate(nodes, rng.integers(0, 2, size=k).astype(np.uint8)))
+    return out
+
+
+@pytest.mark.parametrize("key,q,omega,psi0,seed", [("C1", 4, 8, 400, 1), ("C2", 7, 16, 500, 2)])
+def test_multi_property_driver_matches_oracle(pbn, key, q, omega, psi0, seed):
+    """pbn_run_multi (reading Q13) vs the oracle's multi-property
+    Algorithm 4: identical integer decisions, per-property statistics within
+    1e-9, and each estimate equals the pooled mean of its own meta states."""
+    model = config_model(key)
+    props = _multi_props(model, q, seed)
+    pm = pbn.pbn_load(model)
+    st, res, per, err = pbn.pbn_run_multi(pm, props, omega=omega, psi0=psi0, rhat_threshold=1.1, r=0.02,
+                                          s=0.95, eps=1e-10, seed=seed, max_steps=1 << 22)
+    assert st == 0, err
+    o = odr.parallel_two_state_multi(model, props, seed, omega, psi0, 1.1, 0.02, 0.95, 1e-10, 1 << 22,
+                                     threads=16)
+    assert (res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain) == (
+        o.psi, o.gr_iterations, o.extensions, o.sample_size, o.steps_per_chain)
+    assert close(res.rhat, o.rhat)
+    for g, r in zip(per, o.per_prop):
+        assert (g.status != 0) == r["degenerate"]
+        assert close(g.estimate, r["estimate"], 1e-12)
+        if not r["degenerate"]:
+            assert (g.M, g.N) == (r["M"], r["N"])
+            assert close(g.alpha, r["alpha"]) and close(g.beta, r["beta"])
+    # every property's N is met by the pooled sample (P:524)
+    assert all(g.N <= res.sample_size for g, r in zip(per, o.per_prop) if not r["degenerate"])
