@@ -41,325 +41,14 @@
 #include <cstdint>
 #include <cstdio>
 #include <type_traits>
+#include <vector>
 
 #include "pbn_internal.h"
+#include "pbn_node.cuh"
 
 namespace pbn {
 
 namespace {
-
-constexpr uint32_t FULL = 0xFFFFFFFFu;
-
-__device__ __forceinline__ void mulhilo(uint32_t a, uint32_t m, uint32_t& lo, uint32_t& hi)
-{
-    asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}"
-        : "=r"(lo), "=r"(hi)
-        : "r"(a), "r"(m));
-}
-
-// Philox4x32-10 (Salmon et al., SC'11) with precomputed round keys.
-__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                               const uint32_t* __restrict__ rk)
-{
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        uint32_t lo0, hi0, lo1, hi1;
-        mulhilo(c0, 0xD2511F53u, lo0, hi0);
-        mulhilo(c2, 0xCD9E8D57u, lo1, hi1);
-        const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r];
-        const uint32_t n2 = hi0 ^ c3 ^ rk[2 * r + 1];
-        c1 = lo1;
-        c3 = lo0;
-        c0 = n0;
-        c2 = n2;
-    }
-    return make_uint4(c0, c1, c2, c3);
-}
-
-// The same generator split for the step loop.  With counter (q, chain, t_lo,
-// t_hi), the parts of rounds 1-2 that depend only on (chain, t) are computed
-// once per step (PhiloxStep); philox_quad finishes the 10 rounds for quad q.
-struct PhiloxStep {
-    uint32_t c0r1;   // round-1 output word 0: hi(M1 t_lo) ^ chain ^ k0
-    uint32_t c1r1;   // round-1 output word 1: lo(M1 t_lo)
-    uint32_t hi0r2;  // round-2 hi(M0 c0r1)
-    uint32_t lo0r2;  // round-2 lo(M0 c0r1) = round-2 output word 3
-    uint32_t t_hi;
-};
-
-__device__ __forceinline__ PhiloxStep philox_step(uint32_t chain, uint32_t t_lo, uint32_t t_hi,
-                                                  const uint32_t* __restrict__ rk)
-{
-    PhiloxStep s;
-    uint32_t lo1, hi1;
-    mulhilo(t_lo, 0xCD9E8D57u, lo1, hi1);
-    s.c0r1 = hi1 ^ chain ^ rk[0];
-    s.c1r1 = lo1;
-    mulhilo(s.c0r1, 0xD2511F53u, s.lo0r2, s.hi0r2);
-    s.t_hi = t_hi;
-    return s;
-}
-
-__device__ __forceinline__ uint4 philox_quad(uint32_t q, const PhiloxStep& s, const uint32_t* __restrict__ rk)
-{
-    // round 1 (quad part): (hi0, lo0) = M0 q
-    uint32_t lo0, hi0;
-    mulhilo(q, 0xD2511F53u, lo0, hi0);
-    const uint32_t c2r1 = hi0 ^ s.t_hi ^ rk[1];
-    const uint32_t c3r1 = lo0;
-    // round 2: M0 * c0r1 is per step; M1 * c2r1 per quad
-    uint32_t lo1, hi1;
-    mulhilo(c2r1, 0xCD9E8D57u, lo1, hi1);
-    uint32_t c0 = hi1 ^ s.c1r1 ^ rk[2];
-    uint32_t c1 = lo1;
-    uint32_t c2 = s.hi0r2 ^ c3r1 ^ rk[3];
-    uint32_t c3 = s.lo0r2;
-#pragma unroll
-    for (int r = 2; r < 10; ++r) {
-        uint32_t a0, b0, a1, b1;
-        mulhilo(c0, 0xD2511F53u, a0, b0);
-        mulhilo(c2, 0xCD9E8D57u, a1, b1);
-        const uint32_t n0 = b1 ^ c1 ^ rk[2 * r];
-        const uint32_t n2 = b0 ^ c3 ^ rk[2 * r + 1];
-        c1 = a1;
-        c3 = a0;
-        c0 = n0;
-        c2 = n2;
-    }
-    return make_uint4(c0, c1, c2, c3);
-}
-
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-// shared-memory accessors on 32-bit shared addresses.  State words change
-// every step (volatile: never cached across barriers); image words are
-// immutable (plain asm: the compiler may schedule and CSE them freely).
-__device__ __forceinline__ uint32_t lds32(uint32_t a)
-{
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds32_ro(uint32_t a)
-{
-    uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds16_ro(uint32_t a)
-{
-    uint16_t v;
-    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-    return (uint32_t)v;
-}
-__device__ __forceinline__ uint2 lds64_ro(uint32_t a)
-{
-    uint2 v;
-    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint4 lds128_ro(uint32_t a)
-{
-    uint4 v;
-    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v)
-{
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-// State words of the current buffer.  `asm volatile` keeps them on the right
-// side of the step barriers at the compiler level; the plain ld.shared lets
-// ptxas interleave the loads of different nodes freely.
-__device__ __forceinline__ uint32_t lds32_state(uint32_t a)
-{
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void fence_state(uint32_t&, uint32_t&) {}
-// 16-byte store of four consecutive words by one lane when pred != 0
-__device__ __forceinline__ void sts128_if(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t pred)
-{
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(a),
-        "r"(x), "r"(y), "r"(z), "r"(w), "r"(pred)
-        : "memory");
-}
-__device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, uint32_t pred)
-{
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
-                 "r"(pred)
-                 : "memory");
-}
-
-
-// Image accessors.  SMEM: the staged image was relocated, so every stored
-// offset is already an absolute shared address.  Global: offsets are
-// relative to the image pointer (read-only path).
-template <bool SMEM>
-struct Img {
-    const uint8_t* gbase;  // global address of the image (!SMEM)
-    __device__ __forceinline__ uint4 ld128(uint32_t a) const
-    {
-        if (SMEM) return lds128_ro(a);
-        return __ldg(reinterpret_cast<const uint4*>(gbase + a));
-    }
-    __device__ __forceinline__ uint2 ld64(uint32_t a) const
-    {
-        if (SMEM) return lds64_ro(a);
-        return __ldg(reinterpret_cast<const uint2*>(gbase + a));
-    }
-    __device__ __forceinline__ uint32_t ld32(uint32_t a) const
-    {
-        if (SMEM) return lds32_ro(a);
-        return __ldg(reinterpret_cast<const uint32_t*>(gbase + a));
-    }
-    __device__ __forceinline__ uint32_t ld16(uint32_t a) const
-    {
-        if (SMEM) return lds16_ro(a);
-        return (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(gbase + a));
-    }
-};
-
-// Generic path for nodes outside the fast shape (ell > 4 or theta_max > 6).
-// `old` = address of buffer-0 word of node 0 plus the old buffer's offset.
-template <bool SMEM>
-__device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w, uint32_t u, uint32_t old,
-                                               uint32_t rot)
-{
-    const uint4 sr = img.ld128(w & ~15u);  // {thr, ell, gdesc, 0}
-    uint32_t j = 0;
-    for (uint32_t k = 0; k + 1 < sr.y; ++k) j += (uint32_t)(u > img.ld32(sr.x + 4u * k));
-    const uint4 gd = img.ld128(sr.z + 16u * j);  // {toff, theta, poff, 0}
-    uint32_t idx = 0;
-    for (uint32_t m = 0; m < gd.y; ++m) {
-        const uint32_t off = img.ld32(gd.z + 4u * m);
-        const uint32_t wv = lds32(old + off);
-        idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
-    }
-    const uint32_t tw = img.ld32(gd.x + 4u * (idx >> 5));
-    return (tw >> (idx & 31u)) & 1u;
-}
-
-// idx += B when this lane's bit of the parent word is set: one LOP3 producing a
-// predicate (ALU pipe) and one predicated add.
-template <uint32_t B>
-__device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t lmask)
-{
-    if (B == 0) return;
-    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
-        "@p add.u32 %0, %0, %3;\n\t}"
-        : "+r"(idx)
-        : "r"(wv), "r"(lmask), "n"(B));
-}
-
-// One node of one step for the warp's 32 chains (A4-A7): returns the node's
-// new state word (bit l = chain of lane l) and its gamma word in *gw_out.
-//   sb   state base (shared address of buffer-0 word of node 0; uniform)
-//   OB   byte offset of the OLD buffer (0 or 16, compile time)
-template <bool SMEM, bool PER_NODE, int FT, bool SLOW, uint32_t OB>
-__device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, const uint4 rec, uint32_t i, uint32_t u,
-                                              uint32_t Tp, uint32_t sb, uint32_t lmask, uint32_t rot,
-                                              uint32_t& gw_out)
-{
-    constexpr uint32_t DS = desc_bytes(FT);
-    const uint32_t gw = __ballot_sync(FULL, u < Tp);  // gamma_i(t) = 1 (A4)
-    uint32_t bit;
-    if (!SLOW || (rec.w & 7u) != kSlowNode) {
-        // A5: descriptor of function j = #{k : u > E_k}
-        uint32_t dp = rec.w;
-        if (u > rec.x) dp += DS;
-        if (u > rec.y) dp += DS;
-        if (u > rec.z) dp += DS;
-        // parent state word: absolute (relocated) address in shared-image
-        // launches, state-relative otherwise
-#define SB(x) (SMEM ? (x) : sb + (x))
-        uint32_t tw, idx = 0;
-        if constexpr (FT >= 7) {
-            // descriptor words {a[0..7], table words}: the first FT-5 parents
-            // pick one of the 2^(FT-5) table words (a dependent load), the other
-            // five index within it
-            const uint4 d0 = img.ld128(dp);
-            const uint4 d1 = img.ld128(dp + 16u);
-            const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-            constexpr int S = FT >= 7 ? FT - 5 : 2;
-            uint32_t widx = 0;
-            add_if_bit<(1u << (S - 1)) * 4u>(widx, lds32_state(SB(a[0]) + OB), lmask);
-            add_if_bit<(S > 1 ? 1u << (S - 2) : 0u) * 4u>(widx, lds32_state(SB(a[1]) + OB), lmask);
-            if (S > 2) add_if_bit<4u>(widx, lds32_state(SB(a[2 % FT]) + OB), lmask);
-            add_if_bit<16u>(idx, lds32_state(SB(a[S % 8]) + OB), lmask);
-            add_if_bit<8u>(idx, lds32_state(SB(a[(S + 1) % 8]) + OB), lmask);
-            add_if_bit<4u>(idx, lds32_state(SB(a[(S + 2) % 8]) + OB), lmask);
-            add_if_bit<2u>(idx, lds32_state(SB(a[(S + 3) % 8]) + OB), lmask);
-            add_if_bit<1u>(idx, lds32_state(SB(a[(S + 4) % 8]) + OB), lmask);
-            tw = img.ld32(dp + 32u + widx);
-        } else {
-        // descriptor words {t0, [t1], a[0..FT-1]}: table word(s), then the FT
-        // padded parents' state offsets, MSB first
-        uint32_t tw0, tw1 = 0, a[6];
-        {
-            const uint4 d0 = img.ld128(dp);
-            if (FT == 6) {
-                const uint4 d1 = img.ld128(dp + 16u);
-                tw0 = d0.x; tw1 = d0.y; a[0] = d0.z; a[1] = d0.w;
-                a[2] = d1.x; a[3] = d1.y; a[4] = d1.z; a[5] = d1.w;
-            } else if (FT == 5) {
-                const uint2 d1 = img.ld64(dp + 16u);
-                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1.x; a[4] = d1.y; a[5] = 0;
-            } else if (FT == 4) {
-                const uint32_t d1 = img.ld32(dp + 16u);
-                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1; a[4] = a[5] = 0;
-            } else {
-                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = a[4] = a[5] = 0;
-            }
-        }
-        // A6: gather: parent k contributes bit (FT-1-k) of the table index when
-        // bit `lane` of its state word is set (LOP3 -> predicate, predicated add)
-        // FT = 6: the first (most significant) parent picks the table word
-        // (entries 32-63 in t1), the other five index within it
-        tw = tw0;
-        if (FT == 6) tw = (lds32_state(SB(a[0]) + OB) & lmask) ? tw1 : tw0;
-        constexpr int S = FT == 6 ? 1 : 0;  // first parent handled above
-        constexpr int R = FT - S;          // parents indexing within the word
-        if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(SB(a[S + 0]) + OB), lmask);
-        if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(SB(a[S + 1]) + OB), lmask);
-        if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(SB(a[(S + 2) % 6]) + OB), lmask);
-        if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(SB(a[(S + 3) % 6]) + OB), lmask);
-        if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(SB(a[(S + 4) % 6]) + OB), lmask);
-        }
-        // the table words are stored bit-REVERSED (entry e at bit 31 - (e & 31)),
-        // so the entry is the sign bit of the word shifted left by idx
-        bit = (uint32_t)((int32_t)(tw << idx) < 0);
-#undef SB
-    } else {
-        bit = slow_node_bit<SMEM>(img, rec.w, u, sb + OB, rot);
-    }
-    uint32_t nb = __ballot_sync(FULL, bit != 0u);  // commit (A7)
-    if (PER_NODE) {
-        const uint32_t ow = lds32_state(sb + state_off(i) + OB);
-        nb = (nb & ~gw) | (~ow & gw);
-    }
-    gw_out = gw;
-    return nb;
-}
-
-// node records {E1, E2, E3, w} of one quad
-struct Recs {
-    uint4 r[4];
-};
-template <bool SMEM>
-__device__ __forceinline__ Recs load_recs(const Img<SMEM>& img, uint32_t a)
-{
-    Recs x;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) x.r[k] = img.ld128(a + 16u * k);
-    return x;
-}
 
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
 __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_constant__ TrajParams P)
@@ -570,26 +259,11 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         // software pipeline: the next quad's Philox words are computed while
         // this quad's nodes gather (independent instruction streams)
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
-#ifdef PBN_PREFETCH_REC
-        // the next quad's node records are loaded with its Philox words
-        Recs rc = load_recs(img, nrec + 64u * (uint32_t)q0);
-        for (int q = q0; q < qf; ++q) {
-            uint4 rn;
-            Recs rcn;
-            quad(q, rw, rc, [&] {
-                rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
-                rcn = load_recs(img, nrec + 64u * (uint32_t)(q + 1 < qf ? q + 1 : q));
-            });
-            rw = rn;
-            rc = rcn;
-        }
-#else
         for (int q = q0; q < qf; ++q) {
             uint4 rn;
             quad(q, rw, load_recs(img, nrec + 64u * (uint32_t)q), [&] { rn = philox_quad((uint32_t)(q + 1), ps, P.rk); });
             rw = rn;
         }
-#endif
         if (qf < q1) {  // ragged last quad (n % 4 != 0), node by node
             const int q = qf;
             const uint32_t i0 = 4u * (uint32_t)q;
