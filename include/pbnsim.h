@@ -143,6 +143,11 @@ typedef struct {
  *                (group, chunk of chunk_steps steps) units, state carried
  *                between chunks in a stream-ordered scratch allocation
  *   chunk_steps  persistent chunk length (0 = auto)
+ *   cluster_size 0: chosen per call -- one CTA per 32-chain group when the
+ *                device image fits one CTA's shared memory and there are
+ *                enough groups to fill the GPU, else a thread-block cluster of
+ *                K CTAs per group (each stages 1/K of the image, the state is
+ *                mirrored through distributed shared memory); 1 / K force it
  *   n_props, props  several properties from the same trajectories (the
  *                multi-property reuse of P:507-526): every statistic below is
  *                produced per property, property-major (property p's block
@@ -167,6 +172,8 @@ typedef struct {
     int64_t chunk_steps;
     int32_t n_props;                /* 0: one property, `pred`; 1..PBN_MAX_PROPS:  */
     const pbn_predicate* props;     /*    props[0..n_props-1] (pred ignored)       */
+    int32_t cluster_size;           /* 0 auto; 1 one CTA per group; 2,4,8,16: a    */
+                                    /* cluster of that many CTAs per group         */
 } pbn_sim_args;
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).

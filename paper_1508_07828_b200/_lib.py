@@ -65,7 +65,7 @@ class pbn_sim_args(C.Structure):
                 ("emit_bits", C.c_int32), ("bits_offset", C.c_int64), ("bits_row_words", C.c_int64),
                 ("groups_per_cta", C.c_int32), ("warps_per_group", C.c_int32),
                 ("schedule", C.c_int32), ("chunk_steps", C.c_int64), ("n_props", C.c_int32),
-                ("props", C.c_void_p)]
+                ("props", C.c_void_p), ("cluster_size", C.c_int32)]
 
 
 class pbn_sim_out(C.Structure):

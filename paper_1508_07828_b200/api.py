@@ -154,7 +154,8 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                  step0: int = 0, burn_in: int = 0, batch: int = 0, seed: int = 0, pred=None,
                  init: bool = False, emit_bits: bool = False, bits_offset: int = 0,
                  bits_row_words: int = 0, groups_per_cta: int = 0, warps_per_group: int = 0,
-                 schedule: int = 0, chunk_steps: int = 0, stream=None, props=None) -> None:
+                 schedule: int = 0, chunk_steps: int = 0, stream=None, props=None,
+                 cluster_size: int = 0) -> None:
     """props: a list of q >= 1 predicates evaluated on the same trajectories
     (multi-property reuse); `pred` is then ignored."""
     cp, _keep = _pred(pred)
@@ -170,7 +171,7 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                        emit_bits=int(bool(emit_bits)), bits_offset=bits_offset,
                        bits_row_words=bits_row_words, groups_per_cta=groups_per_cta,
                        warps_per_group=warps_per_group, schedule=schedule, chunk_steps=chunk_steps,
-                       n_props=n_props, props=props_ptr)
+                       n_props=n_props, props=props_ptr, cluster_size=cluster_size)
     o = out.c_struct()
     check(lib().pbn_simulate(model.handle, C.byref(a), C.byref(o), _stream_handle(stream)))
     del keep_props  # the predicate arrays are read synchronously by the call above

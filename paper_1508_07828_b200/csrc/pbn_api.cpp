@@ -15,6 +15,16 @@
 #include "../../include/pbnsim.h"
 #include "pbn_internal.h"
 
+// Sub-images of one cluster size K (pbn_cluster.cu), concatenated on the device.
+struct ClusterImages {
+    int K = 0;
+    uint8_t* d_buf = nullptr;
+    uint32_t off[pbn::kMaxCluster] = {}, bytes[pbn::kMaxCluster] = {}, reloc_off[pbn::kMaxCluster] = {};
+    int32_t reloc_count[pbn::kMaxCluster] = {};
+    int32_t q_lo[pbn::kMaxCluster + 1] = {};
+    uint32_t max_bytes = 0;
+};
+
 struct pbn_model_s {
     int device = 0;
     pbn::ImageLayout L;
@@ -22,6 +32,7 @@ struct pbn_model_s {
     uint32_t Tp = 0;
     uint32_t flags = 0;
     int64_t n_parents = 0;
+    std::vector<ClusterImages> clusters;  // K = 2, 4, 8, 16 (K <= quads)
 };
 
 namespace {
@@ -194,12 +205,18 @@ inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
     return (d->tables[d->tbl_off[f] + (int32_t)(idx >> 5)] >> (idx & 31u)) & 1u;
 }
 
-std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L)
+// Image of the nodes [node_lo, node_hi) (records at local index i - node_lo)
+// for a group state whose quads are qs bytes apart (32: two buffers, pbn_traj;
+// 48: three buffers, pbn_cluster).  The fast width FT and the slow-node
+// count are model-wide, so every sub-image of a cluster uses one kernel.
+std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L, int32_t node_lo = 0,
+                                 int32_t node_hi = -1, uint32_t qs = 32)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
+    if (node_hi < 0) node_hi = n;
     ImageBuilder B;
     std::vector<uint32_t> reloc;  // byte offsets of offset-valued words
-    const uint32_t off_nrec = B.alloc(16u * (size_t)n);
+    const uint32_t off_nrec = B.alloc(16u * (size_t)std::max(node_hi - node_lo, 1));
     std::vector<int32_t> thmax(n, 0);
     std::vector<char> fast(n, 0);
     int32_t max_ell = 0, max_theta = 0, slow = 0, FT = pbn::kFastMinTheta;
@@ -220,7 +237,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
     L->slow_nodes = slow;
     L->fast_theta = FT;
 
-    for (int32_t i = 0; i < n; ++i) {
+    for (int32_t i = node_lo; i < node_hi; ++i) {
         const int32_t f0 = d->fn_off[i], f1 = d->fn_off[i + 1], ell = f1 - f0;
         // selection thresholds E_1..E_{ell-1} (reading Q3)
         std::vector<uint32_t> E;
@@ -244,7 +261,9 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                     T[idx >> 5] |= table_bit(d, f, idx >> (tm - theta)) << (idx & 31u);
                 uint32_t* w = B.u32(off_desc + ds * (uint32_t)j);
                 const uint32_t wbase = off_desc + ds * (uint32_t)j;
-                auto par = [&](int32_t m) { return pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u); };
+                auto par = [&](int32_t m) {
+                    return pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u, qs);
+                };
                 if (tm >= 7) {
                     // {a[0..7] (a[7] padding when FT = 7), table words}
                     for (int32_t m = 0; m < 8; ++m) {
@@ -277,7 +296,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                 const uint32_t off_t = B.alloc(4u * words, 4);
                 for (int32_t w = 0; w < words; ++w) B.u32(off_t)[w] = d->tables[d->tbl_off[f] + w];
                 const uint32_t off_p = B.alloc(4u * (size_t)std::max(theta, 1), 4);
-                for (int32_t m = 0; m < theta; ++m) B.u32(off_p)[m] = pbn::state_off(d->parents[d->par_off[f] + m]);
+                for (int32_t m = 0; m < theta; ++m) B.u32(off_p)[m] = pbn::state_off(d->parents[d->par_off[f] + m], qs);
                 uint32_t* gd = B.u32(off_gd + 16u * j);
                 gd[0] = off_t;
                 gd[1] = (uint32_t)theta;
@@ -295,10 +314,10 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
             reloc.push_back(off_slow + 8u);
             w3 = off_slow | pbn::kSlowNode;
         }
-        uint32_t* rec = B.u32(off_nrec + 16u * i);
+        uint32_t* rec = B.u32(off_nrec + 16u * (uint32_t)(i - node_lo));
         for (int k = 0; k < 3; ++k) rec[k] = k < (int)E.size() ? E[k] : 0xFFFFFFFFu;
         rec[3] = w3;
-        reloc.push_back(off_nrec + 16u * i + 12u);
+        reloc.push_back(off_nrec + 16u * (uint32_t)(i - node_lo) + 12u);
     }
     B.alloc(16);  // tail slack
     L->bytes = (uint32_t)B.buf.size();
@@ -368,6 +387,38 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
         delete m;
         return cuda_status(e, err, errlen, "cudaMemcpy(image)");
     }
+    // sub-images for the cluster kernel: CTA r of a K-cluster owns quads
+    // [Q r / K, Q (r+1) / K) and its nodes' records and descriptors
+    const int32_t nq = (desc->n + 3) / 4;
+    for (int K = 2; K <= pbn::kMaxCluster && K <= nq; K *= 2) {
+        ClusterImages ci;
+        ci.K = K;
+        std::vector<uint8_t> all;
+        for (int r = 0; r <= K; ++r) ci.q_lo[r] = (int32_t)((int64_t)nq * r / K);
+        for (int r = 0; r < K; ++r) {
+            pbn::ImageLayout Lr;
+            const int32_t lo = 4 * ci.q_lo[r], hi = std::min(desc->n, 4 * ci.q_lo[r + 1]);
+            std::vector<uint8_t> sub = build_image(desc, m->Tp, &Lr, lo, hi, 48u);
+            const size_t off = (all.size() + 15) & ~(size_t)15;
+            all.resize(off + sub.size(), 0);
+            std::memcpy(all.data() + off, sub.data(), sub.size());
+            ci.off[r] = (uint32_t)off;
+            ci.bytes[r] = Lr.bytes;
+            ci.reloc_off[r] = Lr.reloc_off;
+            ci.reloc_count[r] = Lr.reloc_count;
+            ci.max_bytes = std::max(ci.max_bytes, Lr.bytes);
+        }
+        if (cudaMalloc(&ci.d_buf, all.size()) != cudaSuccess ||
+            cudaMemcpy(ci.d_buf, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            if (ci.d_buf) cudaFree(ci.d_buf);
+            for (auto& c : m->clusters) cudaFree(c.d_buf);
+            cudaFree(m->d_image);
+            delete m;
+            set_err(err, errlen, "cluster sub-image upload failed");
+            return PBN_E_CUDA;
+        }
+        m->clusters.push_back(ci);
+    }
     *out = m;
     return PBN_OK;
 }
@@ -376,6 +427,7 @@ void pbn_free(pbn_model model)
 {
     if (!model) return;
     if (model->d_image) cudaFree(model->d_image);
+    for (auto& c : model->clusters) cudaFree(c.d_buf);
     delete model;
 }
 
@@ -475,6 +527,64 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
             return PBN_E_CUDA;
     }
     if (a->n_chains == 0) return PBN_OK;
+    if (a->cluster_size < 0 || a->cluster_size > pbn::kMaxCluster) return PBN_E_USAGE;
+    // ---- one CTA per group (K1) or a cluster of K CTAs per group (K1c) ----
+    int smem_optin = 0, sms = 0;
+    if (cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device) != cudaSuccess)
+        return PBN_E_CUDA;
+    const size_t limit = (size_t)smem_optin - 64;
+    const int64_t groups = (a->n_chains + 31) / 32;
+    const bool k1_smem = (size_t)P.L.bytes + (size_t)P.group_words * 4 <= limit;
+    auto fits = [&](const ClusterImages& ci) { return pbn::cluster_smem_bytes(P, ci.max_bytes) <= limit; };
+    const ClusterImages* use = nullptr;
+    if (a->cluster_size >= 2) {
+        for (const auto& ci : m->clusters)
+            if (ci.K == a->cluster_size) use = &ci;
+        if (!use || !fits(*use)) return PBN_E_USAGE;
+    } else if (a->cluster_size == 0 && groups < sms) {
+        // few-chain regime (measured, C5 sweep): one CTA per group would leave
+        // SMs idle, so split each group's nodes over a cluster; with a full
+        // wave of groups the single-CTA kernel is faster even when its image
+        // is read through L1/L2 (profiles/sweep_c5_r1.jsonl)
+        // the largest fitting K whose groups x K CTAs still fit one wave on
+        // the SMs; if even the smallest fitting K does not, that smallest K
+        const ClusterImages* smallest = nullptr;
+        for (const auto& ci : m->clusters) {
+            if (!fits(ci)) continue;
+            if (!smallest) smallest = &ci;
+            if (groups * ci.K <= sms) use = &ci;
+        }
+        if (!use) use = smallest;
+    }
+    if (use) {
+        pbn::ClusterParams C;
+        std::memset(&C, 0, sizeof(C));
+        C.T = P;
+        C.T.image = use->d_buf;
+        C.K = use->K;
+        for (int r = 0; r < use->K; ++r) {
+            C.img_off[r] = use->off[r];
+            C.img_bytes[r] = use->bytes[r];
+            C.reloc_off[r] = use->reloc_off[r];
+            C.reloc_count[r] = use->reloc_count[r];
+        }
+        for (int r = 0; r <= use->K; ++r) C.q_lo[r] = use->q_lo[r];
+        int qmax = 0;
+        for (int r = 0; r < use->K; ++r) qmax = std::max(qmax, use->q_lo[r + 1] - use->q_lo[r]);
+        int W = a->warps_per_group > 0 ? a->warps_per_group : std::min(pbn::kMaxWarpsPerCta, std::max(qmax, 1));
+        W = std::max(W, P.n_props);
+        if (W > pbn::kMaxWarpsPerCta) return PBN_E_USAGE;
+        C.T.warps_per_group = W;
+        const size_t smem = pbn::cluster_smem_bytes(P, use->max_bytes);
+        int active = 0;
+        if (pbn::max_active_clusters(C, W, smem, &active) != 0 || active < 1) {
+            if (a->cluster_size >= 2 || !k1_smem) return PBN_E_USAGE;
+        } else {
+            const int rc = pbn::launch_traj_cluster(C, W, smem, stream);
+            return rc == 0 ? PBN_OK : PBN_E_CUDA;
+        }
+    }
     pbn::LaunchPlan plan;
     const char* why = nullptr;
     int rc = pbn::plan_traj_launch(P, m->device, a->warps_per_group, &plan, &why);

@@ -72,7 +72,8 @@ constexpr uint32_t kRelocState = 0x80000000u;  // relocation entry: add the stat
 // rounded up to 16 bytes
 __host__ __device__ constexpr uint32_t desc_bytes(int FT) { return FT == 3 ? 16u : FT <= 6 ? 32u : FT == 7 ? 48u : 64u; }
 // byte offset of node i's word in buffer 0 of the group state
-__host__ __device__ constexpr uint32_t state_off(uint32_t i) { return 32u * (i >> 2) + 4u * (i & 3u); }
+// (qs = bytes between quads: 32 for two interleaved buffers, 48 for three)
+__host__ __device__ constexpr uint32_t state_off(uint32_t i, uint32_t qs = 32) { return qs * (i >> 2) + 4u * (i & 3u); }
 constexpr int kFastMaxTheta = 8;
 constexpr int kFastMinTheta = 3;
 constexpr int kFastMaxEll = 4;
@@ -130,6 +131,22 @@ struct TrajParams {
     uint32_t* bits;
     unsigned long long* totals;  // [6 x n_props]
 };
+
+// Cluster launch (pbn_cluster.cu): one 32-chain group per cluster of K CTAs,
+// CTA rank r owns quads [q_lo[r], q_lo[r+1]) and stages sub-image r.
+constexpr int kMaxCluster = 16;
+struct ClusterParams {
+    TrajParams T;               // T.image = base of the K concatenated sub-images
+    int32_t K;
+    uint32_t img_off[kMaxCluster];    // byte offset of sub-image r from T.image
+    uint32_t img_bytes[kMaxCluster];  // staged bytes of sub-image r
+    uint32_t reloc_off[kMaxCluster];  // relocation list of r, from its sub-image start
+    int32_t reloc_count[kMaxCluster];
+    int32_t q_lo[kMaxCluster + 1];
+};
+size_t cluster_smem_bytes(const TrajParams& P, uint32_t max_sub_image);
+int launch_traj_cluster(const ClusterParams& C, int warps, size_t smem_bytes, void* stream);
+int max_active_clusters(const ClusterParams& C, int warps, size_t smem_bytes, int* out);
 
 struct LaunchPlan {
     int warps_per_group;

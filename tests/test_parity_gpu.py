@@ -10,7 +10,7 @@ chains that the oracle computes one by one at the full step count.
 import numpy as np
 import pytest
 
-from tests.helpers import compare_chain, gpu_run, oracle_run, pack_states, sample_chain_ids
+from tests.helpers import compare_chain, gpu_run, oracle_run, pack_states, sample_chain_ids, unpack_states
 from oracle import stats as ostats
 from workloads import (CONFIGS, Predicate, config_model, config_predicate, model_from_lists,
                        random_pbn)
@@ -254,3 +254,38 @@ def test_multi_property_equals_single_property_runs(pbn, key, q, chains, steps, 
     last = {k: (m[k][q - 1] if k != "state" else m[k]) for k in ["state"] + FIELDS}
     for j, cid in enumerate(ids):
         compare_chain(last, cid, packed[j], ws[j], steps, 64)
+
+
+@pytest.mark.parametrize("key,K,chains,per_node", [
+    ("C1", 2, 45, False), ("C1", 2, 45, True),
+    ("C2", 2, 70, False), ("C2", 4, 33, True), ("C2", 8, 100, False), ("C2", 16, 64, False),
+])
+def test_cluster_kernel_equals_single_cta(pbn, key, K, chains, per_node):
+    """The cluster kernel (one group per K-CTA cluster, state mirrored through
+    distributed shared memory) gives exactly the single-CTA kernel's outputs:
+    launch-shape independence (A12) across the two kernels."""
+    model = config_model(key)
+    props = random_props(model, 3, np.random.default_rng(K))
+    pm = load(pbn, model, per_node)
+    kw = dict(n_chains=chains, steps=333, burn_in=77, seed=5, batch=40, props=props)
+    a = gpu_run(pm, model, None, cluster_size=1, **kw)
+    b = gpu_run(pm, model, None, cluster_size=K, **kw)
+    for k in ["state"] + FIELDS:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_cluster_kernel_continuation_and_oracle(pbn):
+    """Cluster launches continue chains exactly (init=False, step0 > 0) and
+    match the oracle on every chain."""
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = load(pbn, model)
+    s1 = gpu_run(pm, model, pred, n_chains=40, steps=200, seed=8, cluster_size=4)
+    s2 = gpu_run(pm, model, pred, n_chains=40, steps=250, step0=200, seed=8, init=False, state=s1["state"],
+                 batch=25, cluster_size=8)
+    st, I, ws = oracle_run(model, pred, np.arange(40), steps=450, seed=8)
+    packed = pack_states(st)
+    assert np.array_equal(s2["state"], packed)
+    _, I2, ws2 = oracle_run(model, pred, np.arange(40), steps=250, step0=200, seed=8, batch=25, init=False,
+                            state=unpack_states(s1["state"], model.n))
+    for c in range(40):
+        compare_chain(s2, c, packed[c], ws2[c], 250, 25)
