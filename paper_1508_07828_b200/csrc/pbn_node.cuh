@@ -227,13 +227,14 @@ __device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t 
 // new state word (bit l = chain of lane l) and its gamma word in *gw_out.
 //   sb   state base (shared address of buffer-0 word of node 0; uniform)
 //   OB   byte offset of the OLD buffer (0 or 16, compile time)
-template <bool SMEM, bool PER_NODE, int FT, bool SLOW, uint32_t OB, uint32_t QS = 32>
+template <bool SMEM, bool PER_NODE, int FT, bool SLOW, uint32_t OB, uint32_t QS = 32, bool GW = true>
 __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, const uint4 rec, uint32_t i, uint32_t u,
                                               uint32_t Tp, uint32_t sb, uint32_t lmask, uint32_t rot,
                                               uint32_t& gw_out)
 {
     constexpr uint32_t DS = desc_bytes(FT);
-    const uint32_t gw = __ballot_sync(FULL, u < Tp);  // gamma_i(t) = 1 (A4)
+    // gamma_i(t) = 1 (A4); callers that form it elsewhere (K1's VECTOR path) skip the vote
+    const uint32_t gw = (GW || PER_NODE) ? __ballot_sync(FULL, u < Tp) : 0u;
     uint32_t bit;
     if (!SLOW || (rec.w & 7u) != kSlowNode) {
         // A5: descriptor of function j = #{k : u > E_k}

@@ -232,37 +232,60 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)
+        constexpr bool GWQ = false;  // VECTOR quads form their gamma ballots after the loop
+        uint64_t gmask = 0;  // VECTOR: flagged quads of the current chunk (bit q - qc)
+        int qc = q0;
         auto quad = [&](const int q, const uint4 rw, const Recs& rc, auto&& between) {
             const uint32_t i0 = 4u * (uint32_t)q;
+            // (the quad's perturbation flag is voted first: one convergence
+            // point for all the ballots below)
+            const uint32_t vq = PER_NODE ? 0u : __ballot_sync(FULL, min(min(rw.x, rw.y), min(rw.z, rw.w)) < Tp);
             // the quad's four nodes are independent: compute all, then one
             // 16-byte store commits them (and their gamma words if any)
             uint32_t g0, g1, g2, g3;
             const uint32_t w0 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[0], i0, rw.x, Tp, gbase, lmask, rot, g0);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB, 32, GWQ>(img, rc.r[0], i0, rw.x, Tp, gbase, lmask, rot, g0);
             const uint32_t w1 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[1], i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB, 32, GWQ>(img, rc.r[1], i0 + 1, rw.y, Tp, gbase, lmask, rot, g1);
             const uint32_t w2 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[2], i0 + 2, rw.z, Tp, gbase, lmask, rot, g2);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB, 32, GWQ>(img, rc.r[2], i0 + 2, rw.z, Tp, gbase, lmask, rot, g2);
             const uint32_t w3 =
-                node_word<SMEM, PER_NODE, FT, SLOW, OB>(img, rc.r[3], i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
+                node_word<SMEM, PER_NODE, FT, SLOW, OB, 32, GWQ>(img, rc.r[3], i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
             // the next quad's Philox words: after the votes, in the same basic
             // block as (and interleaved by the scheduler into) this quad's gathers
             between();
             sts128_if(gbase + 32u * (uint32_t)q + NB, w0, w1, w2, w3, lead);
-            if (!PER_NODE) {
-                const uint32_t g = g0 | g1 | g2 | g3;
-                any |= g;
-                // gamma words only when nonzero (rare); the fixup clears them
-                sts128_if(gam + 4u * i0, g0, g1, g2, g3, g & lead);
-            }
+            if (PER_NODE) return;
+            // VECTOR needs the gamma words only of quads where some chain drew a
+            // perturbation (p = 1e-4: ~1 % of quads): flag the quad with one
+            // vote on the lanes' minimum word; the flagged quads' gamma ballots
+            // are formed after the loop (gmask, below)
+            gmask |= (uint64_t)(vq != 0u) << (q - qc);
         };
         // software pipeline: the next quad's Philox words are computed while
-        // this quad's nodes gather (independent instruction streams)
+        // this quad's nodes gather (independent instruction streams); the
+        // quads run in chunks of <= 64 so each chunk's flags fit one mask
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
-        for (int q = q0; q < qf; ++q) {
-            uint4 rn;
-            quad(q, rw, load_recs(img, nrec + 64u * (uint32_t)q), [&] { rn = philox_quad((uint32_t)(q + 1), ps, P.rk); });
-            rw = rn;
+        for (qc = q0; qc < qf; qc += 64) {
+            const int qe = min(qf, qc + 64);
+            gmask = 0;
+            for (int q = qc; q < qe; ++q) {
+                uint4 rn;
+                quad(q, rw, load_recs(img, nrec + 64u * (uint32_t)q),
+                     [&] { rn = philox_quad((uint32_t)(q + 1), ps, P.rk); });
+                rw = rn;
+            }
+            // flagged quads: recompute their words, form and store the gamma ballots
+            while (!PER_NODE && gmask) {
+                const int j = __ffsll((long long)gmask) - 1;
+                gmask &= gmask - 1;
+                const uint32_t q = (uint32_t)(qc + j);
+                const uint4 rq = philox_quad(q, ps, P.rk);
+                const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
+                const uint32_t g2 = __ballot_sync(FULL, rq.z < Tp), g3 = __ballot_sync(FULL, rq.w < Tp);
+                any |= g0 | g1 | g2 | g3;
+                sts128_if(gam + 16u * q, g0, g1, g2, g3, lead);
+            }
         }
         if (qf < q1) {  // ragged last quad (n % 4 != 0), node by node
             const int q = qf;
