@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)
         constexpr bool GWQ = false;  // VECTOR quads form their gamma ballots after the loop
-        uint64_t gmask = 0;  // VECTOR: flagged quads of the current chunk (bit q - qc)
+        uint32_t gpend = 0;  // VECTOR: flags of the current chunk's quads, bit qe-1-q
         int qc = q0;
         auto quad = [&](const int q, const uint4 rw, const Recs& rc, auto&& between) {
             const uint32_t i0 = 4u * (uint32_t)q;
@@ -260,15 +260,15 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             // perturbation (p = 1e-4: ~1 % of quads): flag the quad with one
             // vote on the lanes' minimum word; the flagged quads' gamma ballots
             // are formed after the loop (gmask, below)
-            gmask |= (uint64_t)(vq != 0u) << (q - qc);
+            gpend = gpend * 2u + min(vq, 1u);  // shift in the quad's flag (newest quad = bit 0)
         };
         // software pipeline: the next quad's Philox words are computed while
         // this quad's nodes gather (independent instruction streams); the
-        // quads run in chunks of <= 64 so each chunk's flags fit one mask
+        // quads run in chunks of <= 32 so each chunk's flags fit one word
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
-        for (qc = q0; qc < qf; qc += 64) {
-            const int qe = min(qf, qc + 64);
-            gmask = 0;
+        for (qc = q0; qc < qf; qc += 32) {
+            const int qe = min(qf, qc + 32);
+            gpend = 0;
             for (int q = qc; q < qe; ++q) {
                 uint4 rn;
                 quad(q, rw, load_recs(img, nrec + 64u * (uint32_t)q),
@@ -276,10 +276,10 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
                 rw = rn;
             }
             // flagged quads: recompute their words, form and store the gamma ballots
-            while (!PER_NODE && gmask) {
-                const int j = __ffsll((long long)gmask) - 1;
-                gmask &= gmask - 1;
-                const uint32_t q = (uint32_t)(qc + j);
+            while (!PER_NODE && gpend) {
+                const int j = __ffs((int)gpend) - 1;
+                gpend &= gpend - 1;
+                const uint32_t q = (uint32_t)(qe - 1 - j);
                 const uint4 rq = philox_quad(q, ps, P.rk);
                 const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
                 const uint32_t g2 = __ballot_sync(FULL, rq.z < Tp), g3 = __ballot_sync(FULL, rq.w < Tp);
