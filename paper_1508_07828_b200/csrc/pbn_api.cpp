@@ -249,7 +249,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
         uint32_t w3 = 0;  // nrec[i].w, written last (B.alloc may move the buffer)
         if (fast[i]) {
             const int32_t tm = FT;  // every fast function is padded to the model-wide FT
-            const uint32_t ds = pbn::desc_bytes(FT);
+            const uint32_t ds = pbn::desc_bytes(tm);
             const uint32_t off_desc = B.alloc((size_t)ds * ell, 16);
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;

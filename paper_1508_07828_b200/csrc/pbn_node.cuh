@@ -223,6 +223,72 @@ __device__ __forceinline__ void add_if_bit(uint32_t& idx, uint32_t wv, uint32_t 
         : "r"(wv), "r"(lmask), "n"(B));
 }
 
+// A6 for one fast function: dp = its descriptor; returns the lane's new bit.
+template <bool SMEM, int FT, uint32_t OB>
+__device__ __forceinline__ uint32_t fast_bit(const Img<SMEM>& img, const uint32_t dp, uint32_t sb, uint32_t lmask)
+{
+    // parent state word: absolute (relocated) address in shared-image
+    // launches, state-relative otherwise
+#define SB(x) (SMEM ? (x) : sb + (x))
+    uint32_t tw, idx = 0;
+    if constexpr (FT >= 7) {
+        // descriptor words {a[0..7], table words}: the first FT-5 parents
+        // pick one of the 2^(FT-5) table words (a dependent load), the other
+        // five index within it
+        const uint4 d0 = img.ld128(dp);
+        const uint4 d1 = img.ld128(dp + 16u);
+        const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        constexpr int S = FT >= 7 ? FT - 5 : 2;
+        uint32_t widx = 0;
+        add_if_bit<(1u << (S - 1)) * 4u>(widx, lds32_state(SB(a[0]) + OB), lmask);
+        add_if_bit<(S > 1 ? 1u << (S - 2) : 0u) * 4u>(widx, lds32_state(SB(a[1]) + OB), lmask);
+        if (S > 2) add_if_bit<4u>(widx, lds32_state(SB(a[2 % FT]) + OB), lmask);
+        add_if_bit<16u>(idx, lds32_state(SB(a[S % 8]) + OB), lmask);
+        add_if_bit<8u>(idx, lds32_state(SB(a[(S + 1) % 8]) + OB), lmask);
+        add_if_bit<4u>(idx, lds32_state(SB(a[(S + 2) % 8]) + OB), lmask);
+        add_if_bit<2u>(idx, lds32_state(SB(a[(S + 3) % 8]) + OB), lmask);
+        add_if_bit<1u>(idx, lds32_state(SB(a[(S + 4) % 8]) + OB), lmask);
+        tw = img.ld32(dp + 32u + widx);
+    } else {
+    // descriptor words {t0, [t1], a[0..FT-1]}: table word(s), then the FT
+    // padded parents' state offsets, MSB first
+    uint32_t tw0, tw1 = 0, a[6];
+    {
+        const uint4 d0 = img.ld128(dp);
+        if (FT == 6) {
+            const uint4 d1 = img.ld128(dp + 16u);
+            tw0 = d0.x; tw1 = d0.y; a[0] = d0.z; a[1] = d0.w;
+            a[2] = d1.x; a[3] = d1.y; a[4] = d1.z; a[5] = d1.w;
+        } else if (FT == 5) {
+            const uint2 d1 = img.ld64(dp + 16u);
+            tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1.x; a[4] = d1.y; a[5] = 0;
+        } else if (FT == 4) {
+            const uint32_t d1 = img.ld32(dp + 16u);
+            tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1; a[4] = a[5] = 0;
+        } else {
+            tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = a[4] = a[5] = 0;
+        }
+    }
+    // A6: gather: parent k contributes bit (FT-1-k) of the table index when
+    // bit `lane` of its state word is set (LOP3 -> predicate, predicated add)
+    // FT = 6: the first (most significant) parent picks the table word
+    // (entries 32-63 in t1), the other five index within it
+    tw = tw0;
+    if (FT == 6) tw = (lds32_state(SB(a[0]) + OB) & lmask) ? tw1 : tw0;
+    constexpr int S = FT == 6 ? 1 : 0;  // first parent handled above
+    constexpr int R = FT - S;          // parents indexing within the word
+    if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(SB(a[S + 0]) + OB), lmask);
+    if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(SB(a[S + 1]) + OB), lmask);
+    if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(SB(a[(S + 2) % 6]) + OB), lmask);
+    if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(SB(a[(S + 3) % 6]) + OB), lmask);
+    if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(SB(a[(S + 4) % 6]) + OB), lmask);
+    }
+    // the table words are stored bit-REVERSED (entry e at bit 31 - (e & 31)),
+    // so the entry is the sign bit of the word shifted left by idx
+    return (uint32_t)((int32_t)(tw << idx) < 0);
+#undef SB
+}
+
 // One node of one step for the warp's 32 chains (A4-A7): returns the node's
 // new state word (bit l = chain of lane l) and its gamma word in *gw_out.
 //   sb   state base (shared address of buffer-0 word of node 0; uniform)
@@ -242,66 +308,7 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, const uint4 
         if (u > rec.x) dp += DS;
         if (u > rec.y) dp += DS;
         if (u > rec.z) dp += DS;
-        // parent state word: absolute (relocated) address in shared-image
-        // launches, state-relative otherwise
-#define SB(x) (SMEM ? (x) : sb + (x))
-        uint32_t tw, idx = 0;
-        if constexpr (FT >= 7) {
-            // descriptor words {a[0..7], table words}: the first FT-5 parents
-            // pick one of the 2^(FT-5) table words (a dependent load), the other
-            // five index within it
-            const uint4 d0 = img.ld128(dp);
-            const uint4 d1 = img.ld128(dp + 16u);
-            const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-            constexpr int S = FT >= 7 ? FT - 5 : 2;
-            uint32_t widx = 0;
-            add_if_bit<(1u << (S - 1)) * 4u>(widx, lds32_state(SB(a[0]) + OB), lmask);
-            add_if_bit<(S > 1 ? 1u << (S - 2) : 0u) * 4u>(widx, lds32_state(SB(a[1]) + OB), lmask);
-            if (S > 2) add_if_bit<4u>(widx, lds32_state(SB(a[2 % FT]) + OB), lmask);
-            add_if_bit<16u>(idx, lds32_state(SB(a[S % 8]) + OB), lmask);
-            add_if_bit<8u>(idx, lds32_state(SB(a[(S + 1) % 8]) + OB), lmask);
-            add_if_bit<4u>(idx, lds32_state(SB(a[(S + 2) % 8]) + OB), lmask);
-            add_if_bit<2u>(idx, lds32_state(SB(a[(S + 3) % 8]) + OB), lmask);
-            add_if_bit<1u>(idx, lds32_state(SB(a[(S + 4) % 8]) + OB), lmask);
-            tw = img.ld32(dp + 32u + widx);
-        } else {
-        // descriptor words {t0, [t1], a[0..FT-1]}: table word(s), then the FT
-        // padded parents' state offsets, MSB first
-        uint32_t tw0, tw1 = 0, a[6];
-        {
-            const uint4 d0 = img.ld128(dp);
-            if (FT == 6) {
-                const uint4 d1 = img.ld128(dp + 16u);
-                tw0 = d0.x; tw1 = d0.y; a[0] = d0.z; a[1] = d0.w;
-                a[2] = d1.x; a[3] = d1.y; a[4] = d1.z; a[5] = d1.w;
-            } else if (FT == 5) {
-                const uint2 d1 = img.ld64(dp + 16u);
-                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1.x; a[4] = d1.y; a[5] = 0;
-            } else if (FT == 4) {
-                const uint32_t d1 = img.ld32(dp + 16u);
-                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1; a[4] = a[5] = 0;
-            } else {
-                tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = a[4] = a[5] = 0;
-            }
-        }
-        // A6: gather: parent k contributes bit (FT-1-k) of the table index when
-        // bit `lane` of its state word is set (LOP3 -> predicate, predicated add)
-        // FT = 6: the first (most significant) parent picks the table word
-        // (entries 32-63 in t1), the other five index within it
-        tw = tw0;
-        if (FT == 6) tw = (lds32_state(SB(a[0]) + OB) & lmask) ? tw1 : tw0;
-        constexpr int S = FT == 6 ? 1 : 0;  // first parent handled above
-        constexpr int R = FT - S;          // parents indexing within the word
-        if (R > 0) add_if_bit<1u << (R > 0 ? R - 1 : 0)>(idx, lds32_state(SB(a[S + 0]) + OB), lmask);
-        if (R > 1) add_if_bit<1u << (R > 1 ? R - 2 : 0)>(idx, lds32_state(SB(a[S + 1]) + OB), lmask);
-        if (R > 2) add_if_bit<1u << (R > 2 ? R - 3 : 0)>(idx, lds32_state(SB(a[(S + 2) % 6]) + OB), lmask);
-        if (R > 3) add_if_bit<1u << (R > 3 ? R - 4 : 0)>(idx, lds32_state(SB(a[(S + 3) % 6]) + OB), lmask);
-        if (R > 4) add_if_bit<1u << (R > 4 ? R - 5 : 0)>(idx, lds32_state(SB(a[(S + 4) % 6]) + OB), lmask);
-        }
-        // the table words are stored bit-REVERSED (entry e at bit 31 - (e & 31)),
-        // so the entry is the sign bit of the word shifted left by idx
-        bit = (uint32_t)((int32_t)(tw << idx) < 0);
-#undef SB
+        bit = fast_bit<SMEM, FT, OB>(img, dp, sb, lmask);
     } else {
         bit = slow_node_bit<SMEM>(img, rec.w, u, sb + OB, rot);
     }
