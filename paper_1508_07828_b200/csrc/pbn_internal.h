@@ -99,6 +99,8 @@ struct TrajParams {
     int32_t n_pad;             // n rounded up to a multiple of 4 (u32 words per buffer)
     int32_t state_words;       // ceil(n/32): row stride of the chain-major state
     int32_t warps_per_group;   // one 32-chain group per CTA
+    int32_t node_warps;        // warps [0, node_warps) own quads
+    int32_t stats_warp0;       // warp stats_warp0 + p keeps property p's statistics
     int32_t group_words;       // u32 words of shared memory for the group's state
     uint32_t image_smem_bytes; // 0 when the image is read from global memory
     int64_t n_chains, chain_base, step0, burn_in, steps, batch;
@@ -150,6 +152,8 @@ int max_active_clusters(const ClusterParams& C, int warps, size_t smem_bytes, in
 
 struct LaunchPlan {
     int warps_per_group;
+    int node_warps;
+    int stats_warp0;
     int ctas;
     int threads;
     size_t smem_bytes;

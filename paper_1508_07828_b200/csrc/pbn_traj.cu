@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
     const uint32_t anyw = gbase + 4u * (PER_NODE ? 2 : 3) * P.n_pad;  // [W]
     const uint32_t nrec = SMEM ? sbase : 0u;     // node records start the image
 
-    const int q0 = (int)((int64_t)wg * P.nquads / W);
-    const int q1 = (int)((int64_t)(wg + 1) * P.nquads / W);
+    const int NW = P.node_warps;  // warps >= NW own no quads (statistics only)
+    const int q0 = wg < NW ? (int)((int64_t)wg * P.nquads / NW) : P.nquads;
+    const int q1 = wg < NW ? (int)((int64_t)(wg + 1) * P.nquads / NW) : P.nquads;
     const int nsw = P.state_words;
     const int b0 = (int)((int64_t)wg * nsw / W), b1 = (int)((int64_t)(wg + 1) * nsw / W);
 
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         uint32_t cur = 0;
         uint32_t* scr = P.scratch + group * (int64_t)P.scratch_stride;  // persistent only
         // statistics warp: warp p < n_props owns property p (A8-A10)
-        const int prop = wg;
-        const bool stats = prop < P.n_props;
+        const int prop = wg - P.stats_warp0;
+        const bool stats = prop >= 0 && prop < P.n_props;
         const int64_t pofs = (int64_t)prop * P.n_chains;  // property-major outputs
 
         // ---- per-lane statistics (warp 0) ----
@@ -513,13 +514,17 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
         *why = "network too large: one 32-chain group's state does not fit in shared memory";
         return -1;
     }
-    // every property needs a statistics warp: at least n_props warps
+    // every property needs a statistics warp: warps [0, n_props), shared with
+    // the node work (dedicated statistics warps after the node warps measured
+    // 0.5 % slower on C4: the layout keeps node_warps / stats_warp0 general)
     int Wp = want_warps > 0 ? want_warps : default_warps(P.nquads);
     Wp = std::max(Wp, P.n_props);
     if (Wp > kMaxWarpsPerCta || Wp > std::max(P.nquads, P.n_props)) {
         *why = "warps_per_group must be <= the CTA warp budget and <= max(ceil(n/4), properties)";
         return -1;
     }
+    plan->node_warps = Wp;
+    plan->stats_warp0 = 0;
     plan->warps_per_group = Wp;
     plan->ctas = (int)((P.n_chains + 31) / 32);
     plan->threads = Wp * 32;
@@ -531,6 +536,8 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
 int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* stream)
 {
     P.warps_per_group = plan.warps_per_group;
+    P.node_warps = plan.node_warps;
+    P.stats_warp0 = plan.stats_warp0;
     P.image_smem_bytes = plan.image_in_smem ? P.L.bytes : 0u;
     const void* fn = pick_kernel(plan.image_in_smem, P.per_node != 0, P.L.fast_theta, P.L.slow_nodes > 0);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
