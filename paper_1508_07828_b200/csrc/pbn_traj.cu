@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -163,17 +164,20 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         }
         const bool first_chunk = chunk == 0;
         const bool last_chunk = r_end >= total;
-        const int64_t chain_local = group * 32 + lane;
-        const bool valid = chain_local < P.n_chains;
+        // (kept in 32 bits: few live registers across the step loop -- the
+        // global-image kernel spilled with 64-bit row indices)
+        const uint32_t chain_local = (uint32_t)group * 32u + (uint32_t)lane;
+        const bool valid = (int64_t)chain_local < P.n_chains;
         const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
         // state buffers: word (i, b) at gbase + state_off(i) + 16 b; every
         // chunk starts from buffer 0, `cur` tracks the newest buffer
         uint32_t cur = 0;
-        uint32_t* scr = P.scratch + group * (int64_t)P.scratch_stride;  // persistent only
+        auto scr = [&]() { return P.scratch + group * (int64_t)P.scratch_stride; };  // persistent only
         // statistics warp: warp p < n_props owns property p (A8-A10)
         const int prop = wg - P.stats_warp0;
         const bool stats = prop >= 0 && prop < P.n_props;
-        const int64_t pofs = (int64_t)prop * P.n_chains;  // property-major outputs
+        // property-major output row of this lane's chain
+        auto orow = [&]() { return (int64_t)prop * P.n_chains + chain_local; };
 
         // ---- per-lane statistics (warp 0) ----
         uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0, bcount = 0;
@@ -181,9 +185,9 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         if (!first_chunk) {
             // resume: bit-sliced state words and warp-0 counters from scratch
             __syncthreads();
-            for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr + i));
+            for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr() + i));
             if (stats) {
-                const uint32_t* st = scr + P.n_pad + 8 * 32 * prop + 8 * lane;
+                const uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
                 c1 = __ldcg(st + 0);
                 n01 = __ldcg(st + 1);
                 n10 = __ldcg(st + 2);
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             }
         } else {
             for (int b = b0; b < b1; ++b) {
-                const uint32_t v = valid ? P.state[chain_local * nsw + b] : 0u;
+                const uint32_t v = valid ? P.state[(int64_t)chain_local * nsw + b] : 0u;
                 for (int k = 0; k < 32; ++k) {
                     const int i = 32 * b + k;
                     if (i >= n) break;
@@ -233,14 +237,19 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)
-        constexpr bool GWQ = false;  // VECTOR quads form their gamma ballots after the loop
+        // VECTOR gamma words: with the image in shared memory, quads are flagged
+        // by one vote and their ballots formed after the loop (lazy, C4 +2 %);
+        // with the image read through L1/L2 the per-node ballots are kept
+        // (eager: the flag vote's dependence on the Philox words costs there)
+        constexpr bool LAZY = SMEM && !PER_NODE;
+        constexpr bool GWQ = !LAZY;
         uint32_t gpend = 0;  // VECTOR: flags of the current chunk's quads, bit qe-1-q
         int qc = q0;
         auto quad = [&](const int q, const uint4 rw, const Recs& rc, auto&& between) {
             const uint32_t i0 = 4u * (uint32_t)q;
             // (the quad's perturbation flag is voted first: one convergence
             // point for all the ballots below)
-            const uint32_t vq = PER_NODE ? 0u : __ballot_sync(FULL, min(min(rw.x, rw.y), min(rw.z, rw.w)) < Tp);
+            const uint32_t vq = LAZY ? __ballot_sync(FULL, min(min(rw.x, rw.y), min(rw.z, rw.w)) < Tp) : 0u;
             // the quad's four nodes are independent: compute all, then one
             // 16-byte store commits them (and their gamma words if any)
             uint32_t g0, g1, g2, g3;
@@ -257,18 +266,26 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             between();
             sts128_if(gbase + 32u * (uint32_t)q + NB, w0, w1, w2, w3, lead);
             if (PER_NODE) return;
+            if (!LAZY) {
+                const uint32_t g = g0 | g1 | g2 | g3;
+                any |= g;
+                // gamma words only when nonzero (rare); the fixup clears them
+                sts128_if(gam + 4u * i0, g0, g1, g2, g3, g & lead);
+                return;
+            }
             // VECTOR needs the gamma words only of quads where some chain drew a
             // perturbation (p = 1e-4: ~1 % of quads): flag the quad with one
             // vote on the lanes' minimum word; the flagged quads' gamma ballots
-            // are formed after the loop (gmask, below)
+            // are formed after the loop (gpend, below)
             gpend = gpend * 2u + min(vq, 1u);  // shift in the quad's flag (newest quad = bit 0)
         };
         // software pipeline: the next quad's Philox words are computed while
         // this quad's nodes gather (independent instruction streams); the
         // quads run in chunks of <= 32 so each chunk's flags fit one word
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
-        for (qc = q0; qc < qf; qc += 32) {
-            const int qe = min(qf, qc + 32);
+        // (eager kernels: one chunk spanning all the warp's quads)
+        for (qc = q0; qc < qf; qc += LAZY ? 32 : qf) {
+            const int qe = LAZY ? min(qf, qc + 32) : qf;
             gpend = 0;
             for (int q = qc; q < qe; ++q) {
                 uint4 rn;
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
                 rw = rn;
             }
             // flagged quads: recompute their words, form and store the gamma ballots
-            while (!PER_NODE && gpend) {
+            while (LAZY && gpend) {
                 const int j = __ffs((int)gpend) - 1;
                 gpend &= gpend - 1;
                 const uint32_t q = (uint32_t)(qe - 1 - j);
@@ -342,7 +359,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             if (P.batch > 0) {
                 bacc += b;
                 if (++bcount == P.batch || wpos + 1 == P.steps) {
-                    if (valid) P.batch_sums[(pofs + chain_local) * P.batch_row + wpos / P.batch] = bacc;
+                    if (valid) P.batch_sums[orow() * P.batch_row + wpos / P.batch] = bacc;
                     bacc = 0;
                     bcount = 0;
                 }
@@ -353,7 +370,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
                 const bool word_end = (bpos & 31) == 31;
                 if (word_end || wpos + 1 == P.steps) {
                     if (valid) {
-                        uint32_t* dst = P.bits + (pofs + chain_local) * P.bits_row + (bpos >> 5);
+                        uint32_t* dst = P.bits + orow() * P.bits_row + (bpos >> 5);
                         // the word holding bit bits_offset keeps its lower (earlier)
                         // bits: OR-merge; every other word is overwritten
                         const bool own = (bpos & ~(int64_t)31) >= P.bits_offset;
@@ -374,9 +391,9 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
     if (!last_chunk) {
         // suspend: bit-sliced state and warp-0 counters to scratch, then
         // release chunk c+1 of this group
-        for (int i = tid; i < n; i += blockDim.x) __stcg(scr + i, lds32(gbase + state_off(i) + cur));
+        for (int i = tid; i < n; i += blockDim.x) __stcg(scr() + i, lds32(gbase + state_off(i) + cur));
         if (stats) {
-            uint32_t* st = scr + P.n_pad + 8 * 32 * prop + 8 * lane;
+            uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
             __stcg(st + 0, c1);
             __stcg(st + 1, n01);
             __stcg(st + 2, n10);
@@ -404,7 +421,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
                 if (i >= n) break;
                 v |= ((lds32(gbase + state_off(i) + cur) >> lane) & 1u) << k;
             }
-            if (valid) P.state[chain_local * nsw + b] = v;
+            if (valid) P.state[(int64_t)chain_local * nsw + b] = v;
         }
     }
     if (stats) {
@@ -416,10 +433,10 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             n0from = (uint32_t)(Wn - c1) - (1u - last);
         }
         if (valid) {
-            if (P.c1) P.c1[pofs + chain_local] = c1;
-            if (P.n01) P.n01[pofs + chain_local] = n01;
-            if (P.n10) P.n10[pofs + chain_local] = n10;
-            if (P.first_last) P.first_last[pofs + chain_local] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
+            if (P.c1) P.c1[orow()] = c1;
+            if (P.n01) P.n01[orow()] = n01;
+            if (P.n10) P.n10[orow()] = n10;
+            if (P.first_last) P.first_last[orow()] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
         }
         if (P.totals) {
             unsigned long long v[6];
@@ -508,7 +525,11 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
     const size_t static_smem = 64;  // mbarrier + slack
     const size_t limit = (size_t)smem_optin - static_smem;
     const size_t group_bytes = (size_t)P.group_words * 4;
-    const bool in_smem = (size_t)P.L.bytes + group_bytes <= limit;
+    // PBN_FORCE_GLOBAL_IMAGE=1 (test knob): read the image through L1/L2 even
+    // when it fits shared memory, so small models exercise that kernel too
+    const char* fg = std::getenv("PBN_FORCE_GLOBAL_IMAGE");
+    const bool force_global = fg && fg[0] == '1';
+    const bool in_smem = !force_global && (size_t)P.L.bytes + group_bytes <= limit;
     const size_t img = in_smem ? P.L.bytes : 0;
     if (img + group_bytes > limit) {
         *why = "network too large: one 32-chain group's state does not fit in shared memory";
@@ -517,7 +538,9 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
     // every property needs a statistics warp: warps [0, n_props), shared with
     // the node work (dedicated statistics warps after the node warps measured
     // 0.5 % slower on C4: the layout keeps node_warps / stats_warp0 general)
-    int Wp = want_warps > 0 ? want_warps : default_warps(P.nquads);
+    // (image through L1/L2: as many warps as possible, to cover the L2 latency)
+    int Wp = want_warps > 0 ? want_warps
+                           : in_smem ? default_warps(P.nquads) : std::max(1, std::min(kMaxWarpsPerCta, P.nquads));
     Wp = std::max(Wp, P.n_props);
     if (Wp > kMaxWarpsPerCta || Wp > std::max(P.nquads, P.n_props)) {
         *why = "warps_per_group must be <= the CTA warp budget and <= max(ceil(n/4), properties)";

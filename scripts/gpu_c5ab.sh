@@ -1,0 +1,6 @@
+for V in default libpbnsim_pre.so; do
+  if [ "$V" = default ]; then unset PBN_LIB_VARIANT; else export PBN_LIB_VARIANT=$V; fi
+  for W in 20 32; do
+  echo -n "$V C5 W=$W "; timeout 600 python bench.py --config C5 --chains 16384 --burn-in 0 --window 10000 --steps 2 --warmup 3 --no-cpu-baseline --warps $W 2>/dev/null | grep -o '"value": [0-9.e+]*' | head -1
+  done
+done

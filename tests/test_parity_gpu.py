@@ -289,3 +289,25 @@ def test_cluster_kernel_continuation_and_oracle(pbn):
                             state=unpack_states(s1["state"], model.n))
     for c in range(40):
         compare_chain(s2, c, packed[c], ws2[c], 250, 25)
+
+
+@pytest.mark.parametrize("key,per_node", [("C1", False), ("C2", False), ("C2", True)])
+def test_global_image_kernel_small_models(pbn, key, per_node, monkeypatch):
+    """The K1 variant that reads the image through L1/L2 (used when the image
+    exceeds shared memory, C5) on small models, forced by the test knob
+    PBN_FORCE_GLOBAL_IMAGE: identical to the shared-memory kernel and to the
+    oracle."""
+    model, pred = config_model(key), config_predicate(key)
+    pm = load(pbn, model, per_node)
+    kw = dict(n_chains=70, steps=400, burn_in=50, seed=21, batch=32, cluster_size=1)
+    a = gpu_run(pm, model, pred, **kw)
+    monkeypatch.setenv("PBN_FORCE_GLOBAL_IMAGE", "1")
+    b = gpu_run(pm, model, pred, **kw)
+    monkeypatch.delenv("PBN_FORCE_GLOBAL_IMAGE")
+    for k in ["state"] + FIELDS:
+        assert np.array_equal(a[k], b[k]), k
+    st, I, ws = oracle_run(model, pred, np.arange(70), steps=400, burn_in=50, seed=21, batch=32,
+                           per_node=per_node)
+    packed = pack_states(st)
+    for c in range(70):
+        compare_chain(b, c, packed[c], ws[c], 400, 32)
