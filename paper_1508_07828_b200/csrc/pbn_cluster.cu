@@ -209,17 +209,13 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
             const uint32_t w3 =
                 node_word<true, PER_NODE, FT, SLOW, OB, QS3>(img, rc.r[3], i0 + 3, rw.w, Tp, gbase, lmask, rot, g3);
             between();
-            if (leader) {
-                const uint32_t a = gbase + QS3 * (uint32_t)q + NB;
-                for (uint32_t p = 0; p < K; ++p) st_cluster128(map_peer(a, p), w0, w1, w2, w3);
-            }
+            // lane p < K pushes the quad's words into CTA p's copy: one store
+            // instruction per quad for all the peers (the words are warp-uniform)
+            if (lane < (int)K) st_cluster128(map_peer(gbase + QS3 * (uint32_t)q + NB, (uint32_t)lane), w0, w1, w2, w3);
             if (!PER_NODE) {
                 const uint32_t g = g0 | g1 | g2 | g3;
                 any |= g;
-                if (g && leader) {
-                    const uint32_t a = gam + 4u * i0;
-                    for (uint32_t p = 0; p < K; ++p) st_cluster128(map_peer(a, p), g0, g1, g2, g3);
-                }
+                if (g && lane < (int)K) st_cluster128(map_peer(gam + 4u * i0, (uint32_t)lane), g0, g1, g2, g3);
             }
         };
         uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
@@ -236,23 +232,14 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
                 uint32_t gk;
                 const uint32_t wk = node_word<true, PER_NODE, FT, SLOW, OB, QS3>(
                     img, img.ld128(sbase + 16u * (i0 + k - node_lo)), i0 + k, rr[k], Tp, gbase, lmask, rot, gk);
-                if (leader) {
-                    const uint32_t a = gbase + state_off(i0 + k, QS3) + NB;
-                    for (uint32_t p = 0; p < K; ++p) st_cluster32(map_peer(a, p), wk);
-                }
+                if (lane < (int)K) st_cluster32(map_peer(gbase + state_off(i0 + k, QS3) + NB, (uint32_t)lane), wk);
                 if (!PER_NODE) {
                     any |= gk;
-                    if (gk && leader) {
-                        const uint32_t a = gam + 4u * (i0 + k);
-                        for (uint32_t p = 0; p < K; ++p) st_cluster32(map_peer(a, p), gk);
-                    }
+                    if (gk && lane < (int)K) st_cluster32(map_peer(gam + 4u * (i0 + k), (uint32_t)lane), gk);
                 }
             }
         }
-        if (!PER_NODE && leader) {
-            const uint32_t a = anyw + 4u * (32u * rank + (uint32_t)wg);
-            for (uint32_t p = 0; p < K; ++p) st_cluster32(map_peer(a, p), any);
-        }
+        if (!PER_NODE && lane < (int)K) st_cluster32(map_peer(anyw + 4u * (32u * rank + (uint32_t)wg), (uint32_t)lane), any);
         // publish the step to the cluster (release) and see every peer's (acquire)
         cluster_sync_all();
         if (!PER_NODE) {
