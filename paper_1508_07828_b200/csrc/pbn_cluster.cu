@@ -183,8 +183,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
     __syncthreads();
     cluster_sync_all();
 
-    // peer bases: the same shared offsets in CTA p (p = rank included)
-    uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0, bcount = 0;
+    ChainStats cs;  // statistics of property `prop` (rank 0's statistics warps)
 
     auto step = [&](const int64_t r, auto ob_c) {
         constexpr uint32_t OB = decltype(ob_c)::value;
@@ -262,42 +261,9 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
             __syncthreads();
         }
         if (stats && r > P.burn_in) {
-            uint32_t Iw = FULL;
-            for (int k = 0; k < P.pred_k[prop]; ++k) {
-                const uint32_t w = lds32(gbase + state_off(P.pred_node[prop][k], QS3) + NB);
-                Iw &= P.pred_val[prop][k] ? w : ~w;
-            }
-            const uint32_t b = (Iw >> lane) & 1u;
-            const int64_t wpos = r - P.burn_in - 1;
-            if (wpos == 0) {
-                first = b;
-            } else {
-                n01 += (~prev & b) & 1u;
-                n10 += (prev & ~b) & 1u;
-            }
-            prev = b;
-            c1 += b;
-            if (P.batch > 0) {
-                bacc += b;
-                if (++bcount == P.batch || wpos + 1 == P.steps) {
-                    if (valid) P.batch_sums[(pofs + chain_local) * P.batch_row + wpos / P.batch] = bacc;
-                    bacc = 0;
-                    bcount = 0;
-                }
-            }
-            if (P.emit_bits) {
-                const int64_t bpos = P.bits_offset + wpos;
-                bitw |= b << (bpos & 31);
-                if ((bpos & 31) == 31 || wpos + 1 == P.steps) {
-                    if (valid) {
-                        uint32_t* dst = P.bits + (pofs + chain_local) * P.bits_row + (bpos >> 5);
-                        const bool own = (bpos & ~(int64_t)31) >= P.bits_offset;
-                        if (own) *dst = bitw;
-                        else atomicOr(dst, bitw);
-                    }
-                    bitw = 0;
-                }
-            }
+            const uint32_t b =
+                ChainStats::indicator(P, prop, lane, [&](uint32_t i) { return gbase + state_off(i, QS3) + NB; });
+            cs.record(P, b, r - P.burn_in - 1, valid, pofs + chain_local);
         }
     };
     for (int64_t r = 1; r <= total; r += 3) {
@@ -320,40 +286,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
             if (valid) P.state[chain_local * nsw + b] = v;
         }
     }
-    if (stats) {
-        const uint32_t last = prev;
-        const int64_t Wn = P.steps;
-        uint32_t n0from = 0, n1from = 0;
-        if (Wn > 0) {
-            n1from = c1 - last;
-            n0from = (uint32_t)(Wn - c1) - (1u - last);
-        }
-        if (valid) {
-            if (P.c1) P.c1[pofs + chain_local] = c1;
-            if (P.n01) P.n01[pofs + chain_local] = n01;
-            if (P.n10) P.n10[pofs + chain_local] = n10;
-            if (P.first_last) P.first_last[pofs + chain_local] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
-        }
-        if (P.totals) {
-            unsigned long long v[6];
-            v[0] = valid ? c1 : 0;
-            v[1] = valid ? (unsigned long long)c1 * c1 : 0;
-            v[2] = valid ? n01 : 0;
-            v[3] = valid ? n10 : 0;
-            v[4] = valid ? n0from : 0;
-            v[5] = valid ? n1from : 0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], o);
-            }
-            if (leader) {
-#pragma unroll
-                for (int k = 0; k < 6; ++k)
-                    if (v[k]) atomicAdd(P.totals + 6 * prop + k, v[k]);
-            }
-        }
-    }
+    if (stats) cs.finish(P, prop, valid, pofs + chain_local, leader);
     // no CTA may exit while a peer can still read or write its shared memory
     cluster_sync_all();
 }

@@ -335,5 +335,99 @@ __device__ __forceinline__ Recs load_recs(const Img<SMEM>& img, uint32_t a)
 }
 
 
+// Per-chain statistics of one property over the recorded window (SURVEY
+// §8(a) A8-A10), kept in the registers of the property's statistics warp
+// (lane = chain) and written once at the end of the launch.
+struct ChainStats {
+    uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0, bcount = 0;
+
+    // A8: I_t of the lane's chain = AND of (node, value) pairs over the
+    // bit-sliced new state (word address of node i: word(i))
+    template <typename WordAddr>
+    __device__ __forceinline__ static uint32_t indicator(const TrajParams& P, int prop, int lane, WordAddr word)
+    {
+        uint32_t Iw = FULL;
+        for (int k = 0; k < P.pred_k[prop]; ++k) {
+            const uint32_t w = lds32(word(P.pred_node[prop][k]));
+            Iw &= P.pred_val[prop][k] ? w : ~w;
+        }
+        return (Iw >> lane) & 1u;
+    }
+
+    // A9: window element wpos = b; `row` = the chain's property-major row
+    __device__ __forceinline__ void record(const TrajParams& P, uint32_t b, int64_t wpos, bool valid, int64_t row)
+    {
+        if (wpos == 0) {
+            first = b;
+        } else {
+            n01 += (~prev & b) & 1u;
+            n10 += (prev & ~b) & 1u;
+        }
+        prev = b;
+        c1 += b;
+        if (P.batch > 0) {
+            bacc += b;
+            if (++bcount == P.batch || wpos + 1 == P.steps) {
+                if (valid) P.batch_sums[row * P.batch_row + wpos / P.batch] = bacc;
+                bacc = 0;
+                bcount = 0;
+            }
+        }
+        if (P.emit_bits) {
+            const int64_t bpos = P.bits_offset + wpos;
+            bitw |= b << (bpos & 31);
+            if ((bpos & 31) == 31 || wpos + 1 == P.steps) {
+                if (valid) {
+                    uint32_t* dst = P.bits + row * P.bits_row + (bpos >> 5);
+                    // the word holding bit bits_offset keeps its lower (earlier)
+                    // bits: OR-merge; every other word is overwritten
+                    const bool own = (bpos & ~(int64_t)31) >= P.bits_offset;
+                    if (own) *dst = bitw;
+                    else atomicOr(dst, bitw);
+                }
+                bitw = 0;
+            }
+        }
+    }
+
+    // end of the launch: counters, first/last and (A10) the six u64 totals
+    // with integer atomics (order-independent, exact)
+    __device__ __forceinline__ void finish(const TrajParams& P, int prop, bool valid, int64_t row, bool leader) const
+    {
+        const uint32_t last = prev;
+        const int64_t Wn = P.steps;
+        uint32_t n0from = 0, n1from = 0;
+        if (Wn > 0) {
+            n1from = c1 - last;
+            n0from = (uint32_t)(Wn - c1) - (1u - last);
+        }
+        if (valid) {
+            if (P.c1) P.c1[row] = c1;
+            if (P.n01) P.n01[row] = n01;
+            if (P.n10) P.n10[row] = n10;
+            if (P.first_last) P.first_last[row] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
+        }
+        if (P.totals) {
+            unsigned long long v[6];
+            v[0] = valid ? c1 : 0;
+            v[1] = valid ? (unsigned long long)c1 * c1 : 0;
+            v[2] = valid ? n01 : 0;
+            v[3] = valid ? n10 : 0;
+            v[4] = valid ? n0from : 0;
+            v[5] = valid ? n1from : 0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], o);
+            }
+            if (leader) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k)
+                    if (v[k]) atomicAdd(P.totals + 6 * prop + k, v[k]);
+            }
+        }
+    }
+};
+
 }  // namespace
 }  // namespace pbn

@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         // property-major output row of this lane's chain
         auto orow = [&]() { return (int64_t)prop * P.n_chains + chain_local; };
 
-        // ---- per-lane statistics (warp 0) ----
-        uint32_t c1 = 0, n01 = 0, n10 = 0, first = 0, prev = 0, bacc = 0, bitw = 0, bcount = 0;
+        // ---- per-lane statistics (statistics warps) ----
+        ChainStats cs;
 
         if (!first_chunk) {
             // resume: bit-sliced state words and warp-0 counters from scratch
@@ -188,14 +188,14 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr() + i));
             if (stats) {
                 const uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
-                c1 = __ldcg(st + 0);
-                n01 = __ldcg(st + 1);
-                n10 = __ldcg(st + 2);
-                first = __ldcg(st + 3);
-                prev = __ldcg(st + 4);
-                bacc = __ldcg(st + 5);
-                bitw = __ldcg(st + 6);
-                bcount = __ldcg(st + 7);
+                cs.c1 = __ldcg(st + 0);
+                cs.n01 = __ldcg(st + 1);
+                cs.n10 = __ldcg(st + 2);
+                cs.first = __ldcg(st + 3);
+                cs.prev = __ldcg(st + 4);
+                cs.bacc = __ldcg(st + 5);
+                cs.bitw = __ldcg(st + 6);
+                cs.bcount = __ldcg(st + 7);
             }
         } else if (P.init) {
             // ---- A2: initial state s_0[i] = u(chain, 0, i) >> 31 ----
@@ -339,47 +339,9 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             __syncthreads();
         }
         if (stats && r > P.burn_in) {
-            // A8: property indicator, bit-sliced over the group's chains
-            uint32_t Iw = FULL;
-            for (int k = 0; k < P.pred_k[prop]; ++k) {
-                const uint32_t w = lds32(gbase + state_off(P.pred_node[prop][k]) + NB);
-                Iw &= P.pred_val[prop][k] ? w : ~w;
-            }
-            const uint32_t b = (Iw >> lane) & 1u;
-            const int64_t wpos = r - P.burn_in - 1;
-            // A9: fused per-chain statistics
-            if (wpos == 0) {
-                first = b;
-            } else {
-                n01 += (~prev & b) & 1u;
-                n10 += (prev & ~b) & 1u;
-            }
-            prev = b;
-            c1 += b;
-            if (P.batch > 0) {
-                bacc += b;
-                if (++bcount == P.batch || wpos + 1 == P.steps) {
-                    if (valid) P.batch_sums[orow() * P.batch_row + wpos / P.batch] = bacc;
-                    bacc = 0;
-                    bcount = 0;
-                }
-            }
-            if (P.emit_bits) {
-                const int64_t bpos = P.bits_offset + wpos;
-                bitw |= b << (bpos & 31);
-                const bool word_end = (bpos & 31) == 31;
-                if (word_end || wpos + 1 == P.steps) {
-                    if (valid) {
-                        uint32_t* dst = P.bits + orow() * P.bits_row + (bpos >> 5);
-                        // the word holding bit bits_offset keeps its lower (earlier)
-                        // bits: OR-merge; every other word is overwritten
-                        const bool own = (bpos & ~(int64_t)31) >= P.bits_offset;
-                        if (own) *dst = bitw;
-                        else atomicOr(dst, bitw);
-                    }
-                    bitw = 0;
-                }
-            }
+            // A8 + A9 for this property, bit-sliced over the group's chains
+            const uint32_t b = ChainStats::indicator(P, prop, lane, [&](uint32_t i) { return gbase + state_off(i) + NB; });
+            cs.record(P, b, r - P.burn_in - 1, valid, orow());
         }
     };
     for (int64_t r = r_begin; r <= r_end; r += 2) {
@@ -394,14 +356,14 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         for (int i = tid; i < n; i += blockDim.x) __stcg(scr() + i, lds32(gbase + state_off(i) + cur));
         if (stats) {
             uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
-            __stcg(st + 0, c1);
-            __stcg(st + 1, n01);
-            __stcg(st + 2, n10);
-            __stcg(st + 3, first);
-            __stcg(st + 4, prev);
-            __stcg(st + 5, bacc);
-            __stcg(st + 6, bitw);
-            __stcg(st + 7, bcount);
+            __stcg(st + 0, cs.c1);
+            __stcg(st + 1, cs.n01);
+            __stcg(st + 2, cs.n10);
+            __stcg(st + 3, cs.first);
+            __stcg(st + 4, cs.prev);
+            __stcg(st + 5, cs.bacc);
+            __stcg(st + 6, cs.bitw);
+            __stcg(st + 7, cs.bcount);
         }
         __syncthreads();
         if (tid == 0) {
@@ -424,40 +386,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
             if (valid) P.state[(int64_t)chain_local * nsw + b] = v;
         }
     }
-    if (stats) {
-        const uint32_t last = prev;
-        const int64_t Wn = P.steps;
-        uint32_t n0from = 0, n1from = 0;
-        if (Wn > 0) {
-            n1from = c1 - last;
-            n0from = (uint32_t)(Wn - c1) - (1u - last);
-        }
-        if (valid) {
-            if (P.c1) P.c1[orow()] = c1;
-            if (P.n01) P.n01[orow()] = n01;
-            if (P.n10) P.n10[orow()] = n10;
-            if (P.first_last) P.first_last[orow()] = (uint8_t)((Wn > 0) ? (first | (last << 1)) : 0);
-        }
-        if (P.totals) {
-            unsigned long long v[6];
-            v[0] = valid ? c1 : 0;
-            v[1] = valid ? (unsigned long long)c1 * c1 : 0;
-            v[2] = valid ? n01 : 0;
-            v[3] = valid ? n10 : 0;
-            v[4] = valid ? n0from : 0;
-            v[5] = valid ? n1from : 0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], o);
-            }
-            if (leader) {
-#pragma unroll
-                for (int k = 0; k < 6; ++k)
-                    if (v[k]) atomicAdd(P.totals + 6 * prop + k, v[k]);
-            }
-        }
-    }
+    if (stats) cs.finish(P, prop, valid, orow(), leader);
     }  // work units
 }
 
