@@ -311,3 +311,31 @@ def test_global_image_kernel_small_models(pbn, key, per_node, monkeypatch):
     packed = pack_states(st)
     for c in range(70):
         compare_chain(b, c, packed[c], ws[c], 400, 32)
+
+
+def test_maximum_sizes(pbn):
+    """Largest networks and functions this build accepts: n = PBN_MAX_NODES
+    (16383, state near the shared-memory limit, image through L1/L2), theta =
+    PBN_MAX_THETA (16, generic path) and ell well above the fast path."""
+    big = random_pbn(16383, 1, 2, 0, 2, 1e-3, seed=11)
+    pred = Predicate(np.array([0, 16382], np.uint16), np.array([1, 0], np.uint8))
+    pm = load(pbn, big)
+    g = gpu_run(pm, big, pred, n_chains=40, steps=30, burn_in=5, seed=2, batch=7)
+    ids = [0, 31, 39]
+    st, I, ws = oracle_run(big, pred, ids, steps=30, burn_in=5, seed=2, batch=7)
+    packed = pack_states(st)
+    for k, c in enumerate(ids):
+        compare_chain(g, c, packed[k], ws[k], 30, 7)
+    wide = random_pbn(17, 3, 6, 15, 16, 0.01, seed=12)
+    pred = Predicate(np.array([3], np.uint16), np.array([1], np.uint8))
+    full_compare(pbn, wide, pred, n_chains=35, steps=200, burn_in=20, seed=4, batch=30)
+
+
+@pytest.mark.parametrize("p", [2.0 ** -32, 0.9])
+def test_extreme_perturbation_probabilities(pbn, p):
+    """T_p = floor(p 2^32) at its smallest non-zero value (p = 2^-32) and a
+    perturbation-dominated chain (p = 0.9), both semantics."""
+    model = random_pbn(45, 1, 4, 1, 6, p, seed=13)
+    pred = Predicate(np.array([0, 1], np.uint16), np.array([1, 1], np.uint8))
+    for per_node in (False, True):
+        full_compare(pbn, model, pred, n_chains=40, steps=300, burn_in=10, seed=6, batch=25, per_node=per_node)
