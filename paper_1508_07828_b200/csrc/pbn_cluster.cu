@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
     const int64_t chain_local = group * 32 + lane;
     const bool valid = chain_local < P.n_chains;
     const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
+    const uint32_t vmask = __ballot_sync(FULL, valid);  // lanes holding real chains
     const int prop = wg;
     const bool stats = rank == 0 && prop < P.n_props;
     const int64_t pofs = (int64_t)prop * P.n_chains;
@@ -246,7 +247,8 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_cluster_kernel(const 
             // anywhere take s XOR gamma instead of f(s)
             uint32_t m = 0;
             for (uint32_t k = (uint32_t)lane; k < 32u * K; k += 32u) m |= lds32(anyw + 4u * k);
-            const uint32_t M = __reduce_or_sync(FULL, m);
+            // (lanes past the last chain are never written out: no fix-up for them)
+            const uint32_t M = __reduce_or_sync(FULL, m) & vmask;
             if (M) {
                 for (int i = tid; i < n; i += blockDim.x) {
                     const uint32_t gmm = lds32(gam + 4u * (uint32_t)i);

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         const uint32_t chain_local = (uint32_t)group * 32u + (uint32_t)lane;
         const bool valid = (int64_t)chain_local < P.n_chains;
         const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
+        const uint32_t vmask = __ballot_sync(FULL, valid);  // lanes holding real chains
         // state buffers: word (i, b) at gbase + state_off(i) + 16 b; every
         // chunk starts from buffer 0, `cur` tracks the newest buffer
         uint32_t cur = 0;
@@ -325,7 +326,9 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_c
         __syncthreads();
         if (!PER_NODE) {
             // VECTOR: chains with any gamma take s XOR gamma instead of f(s)
-            const uint32_t M = __reduce_or_sync(FULL, lane < W ? lds32(anyw + 4u * lane) : 0u);
+            // (lanes past the last chain are never written out: their chains
+            // need no fix-up, which skips it on most steps of a ragged group)
+            const uint32_t M = __reduce_or_sync(FULL, lane < W ? lds32(anyw + 4u * lane) : 0u) & vmask;
             if (M) {
                 const int lo = 4 * q0, hi = min(4 * q1, n);
                 for (int i = lo + lane; i < hi; i += 32) {
