@@ -52,6 +52,16 @@ def algorithmic_alu_ops(model) -> float:
     return float(5.0 + ell.mean() + 2.0 * sel_theta.mean() + 2.0 + sel_big.mean() + 1.0)
 
 
+def algorithmic_smem_wavefronts(model) -> float:
+    """Shared-memory wavefronts per node-update the method needs with 32
+    chains bit-sliced per word: one state word per parent of the selected
+    function plus one metadata read, each serving 32 chains."""
+    theta = np.diff(model.par_off).astype(np.float64)
+    node_of_fn = np.repeat(np.arange(model.n), np.diff(model.fn_off))
+    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n)
+    return float((sel_theta.mean() + 1.0) / 32.0)
+
+
 # --------------------------------------------------------------------------
 # clocks during the timed region
 # --------------------------------------------------------------------------
@@ -179,6 +189,7 @@ def run_sweep(args, cfg, model, pred):
     torch.cuda.set_device(0)
     pm = pbn.pbn_load(model)
     ops = algorithmic_alu_ops(model)
+    smem_wf = algorithmic_smem_wavefronts(model)
     peak = SM_COUNT_B200 * ALU_LANES_PER_CLK_PER_SM * 1965.0 * 1e6 / 1e12
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
@@ -317,6 +328,7 @@ def main():
     # ---- roofline of the dominant kernel (K1 traj_kernel; one launch per step) ----
     avg_kernel_s = statistics.mean(kern_ms) / 1e3
     ops = algorithmic_alu_ops(model)
+    smem_wf = algorithmic_smem_wavefronts(model)
     achieved = node_updates_per_step * ops / avg_kernel_s / 1e12       # T ALU-ops/s
     sm_max = 1965.0
     try:
@@ -398,6 +410,15 @@ def main():
                                        f"x {sm_max:.0f} MHz (guide unit counts; sm_max_mhz of "
                                        f"MEASURED_PEAKS.json)",
                          "kernel": "traj_kernel (K1)", "kernel_ms": statistics.mean(kern_ms)},
+            # the secondary bound named by BASELINE's metric: shared-memory
+            # wavefronts, algorithmic demand (theta_sel + 1)/32 per node-update
+            # (metadata broadcast to 32 chains, one state word per selected
+            # parent), peak one wavefront per SM per clock
+            "roofline_smem": {"bound": "smem", "achieved": node_updates_per_step * smem_wf / avg_kernel_s / 1e12,
+                              "peak": SM_COUNT_B200 * sm_max * 1e6 / 1e12, "unit": "T wavefronts/s",
+                              "frac": (node_updates_per_step * smem_wf / avg_kernel_s)
+                              / (SM_COUNT_B200 * sm_max * 1e6),
+                              "wavefronts_per_node_update": smem_wf},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,
