@@ -390,7 +390,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = ncores()
-        steps_s = 25_000 if model.n >= 1000 else 100_000
+        steps_s = 250_000 if model.n >= 1000 else 1_000_000  # ~10-20 s of oracle work
         v, info = oracle_sample(model, pred, cfg.sim_seed, cores, steps_s, cores)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{info['chains']} chains x {info['steps_per_chain']} transitions of "
