@@ -315,10 +315,8 @@ def main():
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
     kern_ms = [a.elapsed_time(b) for a, b in ev]
-    if dist:
-        t = torch.tensor([total_ms, max(kern_ms)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, kmax = float(t[0]), float(t[1])
+    if dist:  # device-timed region: max over ranks (paper_1508_07828_b200.parallel)
+        total_ms = pbn.parallel.max_over_ranks(total_ms)
     clk = clocks.stop() if rank == 0 else None
 
     node_updates_per_step = chains * (burn_in + window) * model.n
@@ -380,9 +378,7 @@ def main():
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t[0])
+            ems = pbn.parallel.max_over_ranks(ems)
         e2e = {"value": world * node_updates_per_step / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "pinned host state -> pbn_simulate -> all outputs to pinned host"}

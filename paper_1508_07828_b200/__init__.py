@@ -28,3 +28,5 @@ from .api import (  # noqa: F401
     alloc_outputs,
     PbnError,
 )
+
+from . import parallel  # noqa: F401,E402  (chain sharding / u64 totals all-reduce across GPUs)
