@@ -301,6 +301,22 @@ typedef struct {
 pbn_status pbn_run(pbn_model model, const pbn_run_args* args, pbn_run_result* res,
                    void* cuda_stream, char* err, size_t errlen);
 
+/* The same driver over chains spread across several GPUs:
+ * this process simulates chains [chain_base, chain_base + omega_local) of
+ * args->omega (global chain ids: the random stream, hence every chain, is the
+ * one of a single-GPU run) and calls allreduce(values, 6, ctx) -- an in-place
+ * sum over all shards of six u64 counts (S1, S2, n01, n10, n0from, n1from),
+ * returning 0 on success -- whenever a decision needs the pooled counts
+ * (Alg 3 line 9; Alg 4 lines 8-10).  All shards take the
+ * same decisions and call allreduce the same number of times.  Two-state
+ * method only (PBN_E_USAGE for Skart, whose batch means would need an
+ * all-gather).  The result is identical to pbn_run over all omega chains. */
+typedef int (*pbn_allreduce_u64_fn)(uint64_t* values, int32_t count, void* ctx);
+
+pbn_status pbn_run_sharded(pbn_model model, const pbn_run_args* args, int64_t chain_base,
+                           int64_t omega_local, pbn_allreduce_u64_fn allreduce, void* ctx,
+                           pbn_run_result* res, void* cuda_stream, char* err, size_t errlen);
+
 /* Several properties from one set of trajectories: Algorithm 3, then
  * Algorithm 4 with the multi-property reuse of samples (reading
  * Q13).  The omega chains are abstracted into n_props meta-state sequences

@@ -121,8 +121,14 @@ pbn_status read_counts(Workspace& ws, Counts* c, std::vector<uint8_t>* fl)
 
 }  // namespace
 
-extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result* res, void* stream, char* err,
-                              size_t errlen)
+// One driver for one GPU (pbn_run) and for a shard of the chains on each of
+// several GPUs (pbn_run_sharded): this process simulates chains
+// [chain_base, chain_base + ol) of omega; every decision is taken on counts
+// pooled by `allreduce` (the only exchange of the method), so
+// all shards take the same branches and issue the same collectives.
+static pbn_status run_impl(pbn_model m, const pbn_run_args* a, int64_t chain_base, int64_t ol,
+                           pbn_allreduce_u64_fn allreduce, void* ctx, pbn_run_result* res, void* stream, char* err,
+                           size_t errlen)
 {
     if (!m || !a || !res) {
         set_err(err, errlen, "null argument");
@@ -141,8 +147,31 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
     pbn_get_model_info(m, &info);
     Workspace ws;
     ws.s = (cudaStream_t)stream;
-    const int64_t omega = a->omega;
-    if (!ws.init(omega, (info.n + 31) / 32, std::max<int64_t>(2 * a->psi0 / 32 + 2, 64))) {
+    const int64_t omega = a->omega;  // all chains (every formula); this shard simulates ol of them
+    if (ol < 1 || chain_base < 0 || chain_base + ol > omega) {
+        set_err(err, errlen, "shard [%lld, %lld) outside the %lld chains", (long long)chain_base,
+                (long long)(chain_base + ol), (long long)omega);
+        return PBN_E_USAGE;
+    }
+    if (allreduce && a->method != PBN_METHOD_TWO_STATE) {
+        set_err(err, errlen, "sharded runs support the two-state method (Skart needs every batch mean)");
+        return PBN_E_USAGE;
+    }
+    // pooled counts of all shards (identity on one GPU)
+    auto pool = [&](const Counts& loc, Counts* out) -> pbn_status {
+        *out = loc;
+        if (!allreduce) return PBN_OK;
+        uint64_t v[6] = {loc.S1, loc.S2, loc.n01, loc.n10, loc.n0from, loc.n1from};
+        if (allreduce(v, 6, ctx) != 0) return PBN_E_CUDA;
+        out->S1 = v[0];
+        out->S2 = v[1];
+        out->n01 = v[2];
+        out->n10 = v[3];
+        out->n0from = v[4];
+        out->n1from = v[5];
+        return PBN_OK;
+    };
+    if (!ws.init(ol, (info.n + 31) / 32, std::max<int64_t>(2 * a->psi0 / 32 + 2, 64))) {
         set_err(err, errlen, "workspace allocation failed");
         return PBN_E_NOMEM;
     }
@@ -153,8 +182,8 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
         if (!ws.ensure_rows((bits_offset + steps + 31) / 32 + 1)) return PBN_E_NOMEM;
         pbn_sim_args sa;
         std::memset(&sa, 0, sizeof(sa));
-        sa.n_chains = omega;
-        sa.chain_base = 0;
+        sa.n_chains = ol;
+        sa.chain_base = chain_base;
         sa.step0 = len;
         sa.burn_in = burn_in;
         sa.steps = steps;
@@ -192,7 +221,9 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
     for (;;) {
         if ((st = read_counts(ws, &c, &fl)) != PBN_OK) return st;
         res->gr_iterations++;
-        pbn_status g = pbn_gelman_rubin(c.S1, c.S2, omega, psi, &rhat, nullptr, nullptr, nullptr);
+        Counts cp;
+        if ((st = pool(c, &cp)) != PBN_OK) return st;
+        pbn_status g = pbn_gelman_rubin(cp.S1, cp.S2, omega, psi, &rhat, nullptr, nullptr, nullptr);
         if (g == PBN_OK && rhat < a->rhat_threshold) break;
         if (4 * psi > a->max_steps) {
             res->rhat = rhat;
@@ -208,8 +239,8 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
 
     // The merged sample: per chain the row bits [disc, ns), ns = psi initially.
     int64_t ns = psi, disc = 0;
-    std::vector<uint8_t> first(omega), last(omega);
-    for (int64_t k = 0; k < omega; ++k) {
+    std::vector<uint8_t> first(ol), last(ol);  // this shard's chains
+    for (int64_t k = 0; k < ol; ++k) {
         first[k] = fl[k] & 1;
         last[k] = (fl[k] >> 1) & 1;
     }
@@ -223,7 +254,9 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
         for (;;) {
             for (;;) {
                 const int64_t L = ns - disc;
-                pbn_status t2 = (L >= 2) ? pbn_two_state(c.n01, c.n0from, c.n10, c.n1from, a->r, a->s, a->eps, &ts)
+                Counts cp;
+                if ((st = pool(c, &cp)) != PBN_OK) return st;
+                pbn_status t2 = (L >= 2) ? pbn_two_state(cp.n01, cp.n0from, cp.n10, cp.n1from, a->r, a->s, a->eps, &ts)
                                          : PBN_E_DEGENERATE;
                 int64_t ext;
                 if (t2 == PBN_OK) {
@@ -242,7 +275,7 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
                 std::vector<uint8_t> fl2;
                 if ((st = read_counts(ws, &d, &fl2)) != PBN_OK) return st;
                 // pooled counts + the boundary pair (last of old, first of new) per chain (Q7)
-                for (int64_t k = 0; k < omega; ++k) {
+                for (int64_t k = 0; k < ol; ++k) {
                     const int a0 = (L > 0) ? last[k] : -1, b0 = fl2[k] & 1;
                     if (a0 == 0) {
                         c.n0from++;
@@ -268,11 +301,11 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
                 psi = ts.M;
                 const int64_t L = std::max<int64_t>(ns - disc, 0);
                 if (disc > ns) disc = ns;
-                st = pbn_recount(ws.bits, omega, ws.row_words, disc, L, 0, nullptr, nullptr, nullptr, ws.fl,
+                st = pbn_recount(ws.bits, ol, ws.row_words, disc, L, 0, nullptr, nullptr, nullptr, ws.fl,
                                  nullptr, ws.totals, ws.s);
                 if (st != PBN_OK) return st;
                 if ((st = read_counts(ws, &c, &fl)) != PBN_OK) return st;
-                for (int64_t k = 0; k < omega; ++k) {
+                for (int64_t k = 0; k < ol; ++k) {
                     first[k] = fl[k] & 1;
                     last[k] = (fl[k] >> 1) & 1;
                 }
@@ -287,7 +320,9 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
         res->psi = psi;
         res->sample_size = omega * (ns - disc);
         res->steps_per_chain = len;
-        res->estimate = (double)c.S1 / (double)res->sample_size;
+        Counts cp;
+        if ((st = pool(c, &cp)) != PBN_OK) return st;
+        res->estimate = (double)cp.S1 / (double)res->sample_size;
         res->ci_lo = res->ci_hi = NAN;
         return PBN_OK;
     }
@@ -409,4 +444,22 @@ extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result
         kappa = std::max(kappa, (new_eta + p - 1) / p);
         eta = kappa * p;
     }
+}
+
+
+extern "C" pbn_status pbn_run(pbn_model m, const pbn_run_args* a, pbn_run_result* res, void* stream, char* err,
+                              size_t errlen)
+{
+    return run_impl(m, a, 0, a ? a->omega : 0, nullptr, nullptr, res, stream, err, errlen);
+}
+
+extern "C" pbn_status pbn_run_sharded(pbn_model m, const pbn_run_args* a, int64_t chain_base, int64_t omega_local,
+                                      pbn_allreduce_u64_fn allreduce, void* ctx, pbn_run_result* res, void* stream,
+                                      char* err, size_t errlen)
+{
+    if (!allreduce) {
+        set_err(err, errlen, "null all-reduce");
+        return PBN_E_USAGE;
+    }
+    return run_impl(m, a, chain_base, omega_local, allreduce, ctx, res, stream, err, errlen);
 }

@@ -59,3 +59,50 @@ def max_over_ranks(x: float, group=None) -> float:
         t = t.cuda()
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.cpu()[0])
+
+
+def run_sharded(model, *, omega: int, psi0: int, rhat_threshold: float = 1.1, r: float = 0.01,
+                s: float = 0.95, eps: float = 1e-10, seed: int = 0, pred=None, max_steps: int = 1 << 26,
+                group=None, stream=None):
+    """Algorithm 3 + Algorithm 4 over `omega` chains sharded across the ranks
+    of `group` (one GPU each): this rank simulates its contiguous block of
+    global chain ids and the pooled counts are summed with one all-reduce of
+    six u64 per decision (pbn_run_sharded, include/pbnsim.h).  Every rank
+    returns the same (status, pbn_run_result, err) as a single-GPU pbn_run
+    over all chains."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from . import _lib as L
+    from .api import _pred, _stream_handle
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    base, count = shard(omega, world, rank)
+    nccl = dist.get_backend(group) == "nccl"
+    state = {"error": None}
+
+    def _allreduce(values, n, ctx):
+        try:
+            v = np.ctypeslib.as_array(values, shape=(n,)).view(np.int64)
+            t = torch.from_numpy(v.copy())
+            if nccl:
+                t = t.cuda()
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            v[:] = t.cpu().numpy()
+            return 0
+        except Exception as e:  # reported through the status, never raised across C
+            state["error"] = e
+            return 1
+
+    cb = L.ALLREDUCE_FN(_allreduce)
+    cp, _keep = _pred(pred)
+    a = L.pbn_run_args(method=0, omega=omega, psi0=psi0, rhat_threshold=rhat_threshold, r=r, s=s, eps=eps,
+                       seed=seed, pred=cp, max_steps=max_steps)
+    res = L.pbn_run_result()
+    err = C.create_string_buffer(512)
+    st = L.lib().pbn_run_sharded(model.handle, C.byref(a), base, count, C.cast(cb, C.c_void_p), None,
+                                 C.byref(res), _stream_handle(stream), err, 512)
+    msg = err.value.decode(errors="replace")
+    if state["error"] is not None:
+        msg = f"all-reduce failed: {state['error']}"
+    return st, res, msg

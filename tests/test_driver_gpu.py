@@ -127,3 +127,48 @@ def test_multi_property_driver_matches_oracle(pbn, key, q, omega, psi0, seed):
             assert close(g.alpha, r["alpha"]) and close(g.beta, r["beta"])
     # every property's N is met by the pooled sample
     assert all(g.N <= res.sample_size for g, r in zip(per, o.per_prop) if not r["degenerate"])
+
+
+def _sharded_rank(rank, world, port, outdir):
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_1508_07828_b200 as pbn
+    from workloads import config_model, config_predicate
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    pm = pbn.pbn_load(config_model("C2"))
+    st, res, err = pbn.parallel.run_sharded(pm, omega=24, psi0=500, rhat_threshold=1.1, r=0.02, s=0.95,
+                                            eps=1e-10, seed=7, pred=config_predicate("C2"))
+    np.save(os.path.join(outdir, f"r{rank}.npy"),
+            np.array([st, res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain,
+                      res.M, res.N, res.estimate, res.rhat, res.alpha, res.beta], dtype=np.float64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_driver_equals_single_gpu_run(pbn):
+    """pbn_run_sharded (chains split over 2 ranks, 6-u64 all-reduce per
+    decision over gloo; both ranks on this GPU -- a functional check of the
+    multi-GPU driver, not a performance run) gives every decision and
+    statistic of the single-GPU pbn_run over all chains."""
+    import socket
+    import tempfile
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_sharded_rank, args=(2, port, d), nprocs=2, join=True)
+        got = [np.load(f"{d}/r{r}.npy") for r in range(2)]
+    pm = pbn.pbn_load(config_model("C2"))
+    st, res, err = pbn.pbn_run(pm, method=0, omega=24, psi0=500, rhat_threshold=1.1, r=0.02, s=0.95,
+                               eps=1e-10, seed=7, pred=config_predicate("C2"))
+    assert st == 0, err
+    ref = np.array([st, res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain,
+                    res.M, res.N, res.estimate, res.rhat, res.alpha, res.beta], dtype=np.float64)
+    for g in got:
+        assert np.array_equal(g, ref), (g, ref)
