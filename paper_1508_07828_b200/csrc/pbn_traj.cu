@@ -51,8 +51,18 @@ namespace pbn {
 
 namespace {
 
+// Thread budget of the global-image kernels (image through L1/L2, 64-bit
+// image addresses): 896 threads = 28 warps at 72 registers, no spills in the
+// quad loop (C5, 16384 chains: 3.13e11 vs 2.88e11 node-updates/s with 32 warps
+// at 64 registers and local-memory reloads in the loop; 24 warps: 2.90e11)
+#ifndef PBN_GLOBAL_THREADS
+#define PBN_GLOBAL_THREADS 896
+#endif
+constexpr int kGlobalImageThreads = PBN_GLOBAL_THREADS < PBN_MAX_THREADS ? PBN_GLOBAL_THREADS : PBN_MAX_THREADS;
+
 template <bool SMEM, bool PER_NODE, int FT, bool SLOW>
-__global__ void __launch_bounds__(PBN_MAX_THREADS, 1) traj_kernel(const __grid_constant__ TrajParams P)
+__global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 1)
+    traj_kernel(const __grid_constant__ TrajParams P)
 {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -472,7 +482,8 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
     // 0.5 % slower on C4: the layout keeps node_warps / stats_warp0 general)
     // (image through L1/L2: as many warps as possible, to cover the L2 latency)
     int Wp = want_warps > 0 ? want_warps
-                           : in_smem ? default_warps(P.nquads) : std::max(1, std::min(kMaxWarpsPerCta, P.nquads));
+                           : in_smem ? default_warps(P.nquads)
+                                     : std::max(1, std::min(kGlobalImageThreads / 32, P.nquads));
     Wp = std::max(Wp, P.n_props);
     if (Wp > kMaxWarpsPerCta || Wp > std::max(P.nquads, P.n_props)) {
         *why = "warps_per_group must be <= the CTA warp budget and <= max(ceil(n/4), properties)";
