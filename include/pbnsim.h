@@ -138,7 +138,7 @@ typedef struct {
  *                touched word is overwritten
  *   bits_row_words  row stride of `bits` in u32 (0 = ceil(steps/32))
  *   groups_per_cta  0 or 1 (one 32-chain group per CTA in this build)
- *   warps_per_group warps sharing one group's nodes (0 = auto, <= 32)
+ *   warps_per_group warps sharing one group's nodes (0 = auto, <= 28 in this build)
  *   schedule     0 auto; 1 one CTA per group; 2 persistent CTAs pulling
  *                (group, chunk of chunk_steps steps) units, state carried
  *                between chunks in a stream-ordered scratch allocation

@@ -62,8 +62,10 @@ constexpr int kMaxProps = 8;   // properties per launch (multi-proper
 // threads per CTA the trajectory kernel is compiled for (register budget
 // 65536 / threads per thread); one 32-chain group's nodes are split over
 // these warps
+// 896 = 28 warps at 72 registers: C4 (20 warps x 25 quads) 5.33e11 vs 5.28e11
+// node-updates/s with the 64 registers of a 1024-thread budget
 #ifndef PBN_MAX_THREADS
-#define PBN_MAX_THREADS 1024
+#define PBN_MAX_THREADS 896
 #endif
 constexpr int kMaxWarpsPerCta = PBN_MAX_THREADS / 32;
 constexpr uint32_t kSlowNode = 7;   // nrec.w low bits marking a slow node
