@@ -549,9 +549,11 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         // is read through L1/L2 (profiles/sweep_c5_r1.jsonl)
         // the largest fitting K whose groups x K CTAs still fit one wave on
         // the SMs; if even the smallest fitting K does not, that smallest K
+        // (each CTA keeps >= 3 quads: below that the per-step cluster barrier
+        // dominates -- C2, 25 quads: K = 8 beats K = 16 by 20 %)
         const ClusterImages* smallest = nullptr;
         for (const auto& ci : m->clusters) {
-            if (!fits(ci)) continue;
+            if (!fits(ci) || 3 * ci.K > (P.n + 3) / 4) continue;
             if (!smallest) smallest = &ci;
             if (groups * ci.K <= sms) use = &ci;
         }

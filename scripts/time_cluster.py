@@ -5,11 +5,14 @@ import torch
 import paper_1508_07828_b200 as pbn
 from workloads import config_model, config_predicate
 torch.cuda.set_device(0)
-model, pred = config_model("C5"), config_predicate("C5")
+key = sys.argv[1] if len(sys.argv) > 1 else "C5"
+model, pred = config_model(key), config_predicate(key)
 pm = pbn.pbn_load(model)
 steps = 2000
 for chains in (1, 64, 1024):
     for K in (1, 2, 4, 8, 16):
+        if K > (model.n + 3) // 4:
+            continue
         out = pbn.alloc_outputs(pm, chains, steps, batch=100, emit_bits=True)
         def run():
             pbn.pbn_simulate(pm, out, n_chains=chains, steps=steps, batch=100, seed=5, pred=pred, init=True,
@@ -21,4 +24,4 @@ for chains in (1, 64, 1024):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); run(); b.record(); torch.cuda.synchronize()
         ms = a.elapsed_time(b)
-        print(chains, K, f"{ms:.2f} ms", f"{chains * steps * model.n / ms / 1e-3:.3g} node-updates/s", flush=True)
+        print(key, chains, K, f"{ms:.2f} ms", f"{chains * steps * model.n / ms / 1e-3:.3g} node-updates/s", flush=True)
