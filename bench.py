@@ -117,6 +117,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def ncores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -390,7 +401,8 @@ def main():
         v, info = oracle_sample(model, pred, cfg.sim_seed, cores, steps_s, cores)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{info['chains']} chains x {info['steps_per_chain']} transitions of "
-                         f"{cfg.key} ({info['seconds']:.1f} s wall, one thread per chain)"}
+                         f"{cfg.key} ({info['seconds']:.1f} s wall, one thread per chain)",
+               "per_core": v / cores, "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
