@@ -542,11 +542,12 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         for (const auto& ci : m->clusters)
             if (ci.K == a->cluster_size) use = &ci;
         if (!use || !fits(*use)) return PBN_E_USAGE;
-    } else if (a->cluster_size == 0 && groups < sms) {
-        // few-chain regime (measured, C5 sweep): one CTA per group would leave
-        // SMs idle, so split each group's nodes over a cluster; with a full
-        // wave of groups the single-CTA kernel is faster even when its image
-        // is read through L1/L2 (profiles/sweep_c5_r1.jsonl)
+    } else if (a->cluster_size == 0 && 2 * groups <= sms) {
+        // few-chain regime: one CTA per group would leave at least half the
+        // SMs idle, so split each group's nodes over a cluster (measured: C3,
+        // 64 groups: K = 2 1.6x the single-CTA kernel; 128 groups: single-CTA
+        // 1.24x K = 2; with a full wave the single-CTA kernel wins even when
+        // its image is read through L1/L2, profiles/sweep_c5_r1.jsonl)
         // the largest fitting K whose groups x K CTAs still fit one wave on
         // the SMs; if even the smallest fitting K does not, that smallest K
         // (each CTA keeps >= 3 quads: below that the per-step cluster barrier
