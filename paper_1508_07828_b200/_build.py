@@ -32,13 +32,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (), out: str | None = None) -> str:
+def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (), out: str | None = None,
+          extra: tuple[str, ...] = ()) -> str:
     """Compile libpbnsim.so (or, for A/B experiments, a variant `out` with extra -D defines)."""
     lib = os.path.join(HERE, out) if out else LIB
     if not force and not out and not _stale():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", *[f"-D{d}" for d in defines],
+    cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", *[f"-D{d}" for d in defines], *extra,
            "-Xcompiler", "-fPIC,-O3", "-shared", "-I", os.path.join(ROOT, "include"),
            "-o", tmp, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
