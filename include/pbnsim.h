@@ -141,8 +141,9 @@ typedef struct {
  *   warps_per_group warps sharing one group's nodes (0 = auto, <= 28 in this build)
  *   schedule     0 auto; 1 one CTA per group; 2 persistent CTAs pulling
  *                (group, chunk of chunk_steps steps) units, state carried
- *                between chunks in a stream-ordered scratch allocation
+ *                between chunks in `workspace`
  *   chunk_steps  persistent chunk length (0 = auto)
+ *   workspace    caller-owned device scratch (see pbn_simulate_workspace_size)
  *   cluster_size 0: chosen per call -- one CTA per 32-chain group when the
  *                device image fits one CTA's shared memory and there are
  *                enough groups to fill the GPU, else a thread-block cluster of
@@ -174,6 +175,8 @@ typedef struct {
     const pbn_predicate* props;     /*    props[0..n_props-1] (pred ignored)       */
     int32_t cluster_size;           /* 0 auto; 1 one CTA per group; 2,4,8,16: a    */
                                     /* cluster of that many CTAs per group         */
+    void* workspace;                /* caller-owned DEVICE scratch of at least     */
+    int64_t workspace_bytes;        /* pbn_simulate_workspace_size() bytes, or NULL */
 } pbn_sim_args;
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).
@@ -210,6 +213,16 @@ typedef struct {
  * large for shared memory), PBN_E_CUDA (launch failure). */
 pbn_status pbn_simulate(pbn_model model, const pbn_sim_args* args, const pbn_sim_out* out,
                         void* cuda_stream);
+
+/* Device scratch a pbn_simulate call with these args may need (the
+ * persistent schedule suspends each 32-chain group's bit-sliced state and
+ * counters between step chunks): *bytes = 0 when none can be needed.  Only
+ * n_chains and n_props of `args` are read.  Passing a buffer of at least this
+ * size as args->workspace makes pbn_simulate allocation-free; with
+ * workspace = NULL a persistent launch makes one stream-ordered
+ * cudaMallocAsync/cudaFreeAsync pair.  A workspace is used by one call at a
+ * time (calls on one stream may share it).  PBN_E_USAGE for bad arguments. */
+pbn_status pbn_simulate_workspace_size(pbn_model model, const pbn_sim_args* args, int64_t* bytes);
 
 /* Recount (K2) window statistics of a sub-window [start, start+length) of a
  * stored indicator bitstream (device) without re-simulation: used by the
@@ -268,6 +281,40 @@ typedef struct {
 pbn_status pbn_skart_ci_from_batches(const uint32_t* batch_sums, int64_t omega, int64_t per_chain,
                                      int64_t kappa, double alpha_conf, pbn_skart_ci* res);
 
+/* Skart sample sizing (Alg 5 lines 3-21; Alg 2) over
+ * the pooled 0/1 indicator samples of omega converged chains held as DEVICE
+ * bitstreams: chain c's sample element w is bit (start + w) of row c of
+ * `bits` (row stride row_words u32, layout of pbn_sim_out.bits), the first
+ * `available` elements of every row are valid.  Batches never straddle
+ * chains (p is rounded up to a multiple of omega, Fig. 2b); batch
+ * sums come from K2 recounts of the bits.  Declared Skart constants per SPEC
+ * S:375 (reading Q11), chain-major batch means without cross-chain pairs
+ * (Q12).  Returns
+ *   PBN_OK               the CI meets H <= h_star: res complete;
+ *   PBN_E_NOT_CONVERGED  res->need_per_chain > available: extend every chain
+ *                        to that many samples and call again (the machine
+ *                        replays its decisions on the unchanged prefix, so
+ *                        repeated calls take the decisions of one pass);
+ *                        need_per_chain = 0: an iteration cap (64) was hit;
+ *   PBN_E_USAGE / PBN_E_CUDA / PBN_E_NOMEM.
+ * Synchronises `cuda_stream` (batch sums are read back to the host). */
+typedef struct {
+    double estimate;         /* grand mean of the batch means mu              */
+    double ci_lo, ci_hi;     /* skewness- and autoregression-adjusted CI      */
+    double H;                /* max(mu - ci_lo, ci_hi - mu) <= h_star         */
+    double skew;             /* skewness of the first 1280 samples (line 5)   */
+    int64_t kappa;           /* final batch size                              */
+    int64_t batches;         /* final batch count p (multiple of omega)       */
+    int64_t spacer;          /* final spacer d (randomness-test failures)     */
+    int64_t eta;             /* kappa * p samples used                        */
+    int64_t need_per_chain;  /* PBN_E_NOT_CONVERGED: samples per chain needed */
+    int32_t randomness_tests;
+} pbn_skart_result;
+
+pbn_status pbn_skart(const uint32_t* bits, int64_t omega, int64_t row_words, int64_t start,
+                     int64_t available, double h_star, double alpha_conf, pbn_skart_result* res,
+                     void* cuda_stream);
+
 /* -------------------------------------------------------------------- */
 /* Host driver: Algorithm 3 then Algorithm 4 or 5           */
 /* -------------------------------------------------------------------- */
@@ -293,8 +340,9 @@ typedef struct {
     int64_t sample_size;     /* pooled elements used by the estimate             */
     int64_t steps_per_chain; /* total transitions simulated per chain            */
     int64_t gr_iterations;
-    int64_t extensions;
-    int64_t M, N;            /* last two-state burn-in / sample size             */
+    int64_t extensions;      /* two-state: Alg 4 extensions; Skart: final spacer d */
+    int64_t M, N;            /* two-state: last burn-in M / sample size N;       */
+                             /* Skart: final batch size kappa / batch count p    */
     double alpha, beta;
 } pbn_run_result;
 
@@ -304,13 +352,20 @@ pbn_status pbn_run(pbn_model model, const pbn_run_args* args, pbn_run_result* re
 /* The same driver over chains spread across several GPUs:
  * this process simulates chains [chain_base, chain_base + omega_local) of
  * args->omega (global chain ids: the random stream, hence every chain, is the
- * one of a single-GPU run) and calls allreduce(values, 6, ctx) -- an in-place
- * sum over all shards of six u64 counts (S1, S2, n01, n10, n0from, n1from),
- * returning 0 on success -- whenever a decision needs the pooled counts
- * (Alg 3 line 9; Alg 4 lines 8-10).  All shards take the
- * same decisions and call allreduce the same number of times.  Two-state
- * method only (PBN_E_USAGE for Skart, whose batch means would need an
- * all-gather).  The result is identical to pbn_run over all omega chains. */
+ * one of a single-GPU run; omega_local >= 1 on every shard) and calls
+ * allreduce(values, count, ctx) -- an in-place element-wise sum over all
+ * shards of `count` u64 values, returning 0 on success -- whenever a decision
+ * needs pooled numbers.  values[0] is an error flag (a shard that failed
+ * locally sends 1 and returns; every other shard then returns PBN_E_CUDA
+ * instead of waiting in a collective the failed shard never reaches); the
+ * rest are, for the two-state method and the Gelman & Rubin loop, the six
+ * counts (S1, S2, n01, n10, n0from, n1from) (Alg 3 line 9; Alg 4
+ * lines 8-10), and for Skart the all-gather of the per-chain
+ * batch sums [omega x per_chain] (chain-major; each shard fills its own rows,
+ * the others are 0; batches never straddle chains, Fig. 2b).  All
+ * shards take the same decisions and call allreduce the same number of times
+ * with the same counts.  The result is identical to pbn_run over all omega
+ * chains. */
 typedef int (*pbn_allreduce_u64_fn)(uint64_t* values, int32_t count, void* ctx);
 
 pbn_status pbn_run_sharded(pbn_model model, const pbn_run_args* args, int64_t chain_base,

@@ -10,6 +10,13 @@ Q8 Gelman-Rubin details, Q9 Algorithm 4 garbles, Q11/Q12 Skart constants.
 Chain bookkeeping: `seq[c]` holds the indicator of chain c for every state
 after the Gelman-Rubin burn-in, i.e. states s_{psi+1}, s_{psi+2}, ... of the
 final GR length 2 psi (the GR window first, then every extension).
+
+Sample source: by default the oracle simulator (`Chains`).  Any object with
+the same two members -- `length` (transitions simulated per chain) and
+`advance(burn_in, steps) -> I [omega x steps]` (the indicator of the
+recorded states) -- can stand in for it, e.g. an i.i.d. Bernoulli stream in
+the Skart pins.  The decisions below only ever look at the
+indicator sequences the source returns.
 """
 from __future__ import annotations
 
@@ -81,18 +88,23 @@ def generate_converged_chains(ch: Chains, psi0: int, threshold: float, max_steps
 
 
 def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold: float, r: float,
-                       s: float, eps: float, max_steps: int, threads: int = 8) -> RunResult:
+                       s: float, eps: float, max_steps: int, threads: int = 8, source=None) -> RunResult:
     """Algorithm 4 with reading Q9: extend by ceil((N - omega n)/omega)
     while N > omega n; then if M > psi discard M - psi more initial elements of
-    every chain's sample, set psi := M and re-enter; stop when M <= psi."""
-    ch = Chains(model, pred, seed, omega, threads)
+    every chain's sample, set psi := M and re-enter; stop when M <= psi.
+
+    "additional M - psi elements will be discarded in the beginning of each
+    chain": when that is more than the current sample holds, the
+    sample is empty and the discard continues into the next extension (the
+    discarded prefix is never shortened)."""
+    ch = source if source is not None else Chains(model, pred, seed, omega, threads)
     psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
     seq = [[int(v) for v in window[c]] for c in range(omega)]   # per-chain sample (GR window first)
     disc = 0                                         # elements discarded at the front
     ext_count = 0
     while True:
         while True:
-            L = len(seq[0]) - disc
+            L = max(len(seq[0]) - disc, 0)
             counts = ost.estimate_alpha_beta([np.asarray(x[disc:]) for x in seq]) if L >= 2 else None
             ts = ost.two_state(*counts, r, s, eps) if counts is not None else None
             if ts is not None and not ts.degenerate:
@@ -110,7 +122,6 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
         if ts.M > psi:
             disc += ts.M - psi
             psi = ts.M
-            disc = min(disc, len(seq[0]))
             continue
         break
     L = len(seq[0]) - disc
@@ -135,7 +146,8 @@ class MultiResult:
 
 
 def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, threshold: float, r: float,
-                             s: float, eps: float, max_steps: int, threads: int = 8) -> MultiResult:
+                             s: float, eps: float, max_steps: int, threads: int = 8,
+                             sources=None) -> MultiResult:
     """q properties checked on one set of omega trajectories.
 
     "The simulated samples are abstracted into different meta states based on
@@ -150,7 +162,7 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
     not drive the extension.  Burn-in re-check with the largest
     M_p (reading Q9)."""
     q = len(preds)
-    chs = [Chains(model, pr, seed, omega, threads) for pr in preds]
+    chs = sources if sources is not None else [Chains(model, pr, seed, omega, threads) for pr in preds]
     psi = psi0
     windows = [ch.advance(psi, psi) for ch in chs]
     it = 0
@@ -171,7 +183,7 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
     disc, ext_count = 0, 0
     while True:
         while True:
-            L = len(seqs[0][0]) - disc
+            L = max(len(seqs[0][0]) - disc, 0)
             ts = []
             for p in range(q):
                 counts = ost.estimate_alpha_beta([np.asarray(x[disc:]) for x in seqs[p]]) if L >= 2 else None
@@ -196,7 +208,6 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
         if Mmax > psi:
             disc += Mmax - psi
             psi = Mmax
-            disc = min(disc, len(seqs[0][0]))
             continue
         break
     L = len(seqs[0][0]) - disc
@@ -264,8 +275,11 @@ def batch_sums(seq: list, start: int, kappa: int, per_chain: int) -> np.ndarray:
 
 
 def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: float, h_star: float,
-                   alpha_conf: float, max_steps: int, threads: int = 8) -> RunResult:
-    ch = Chains(model, pred, seed, omega, threads)
+                   alpha_conf: float, max_steps: int, threads: int = 8, source=None) -> RunResult:
+    """Algorithm 5 with SPEC's declared Skart constants (reading
+    Q11) and omega-rounded batch counts (Q12).  `trace` lists, per randomness
+    test, (kappa, p, d, z, passed) and finally ("ci", kappa, p, d)."""
+    ch = source if source is not None else Chains(model, pred, seed, omega, threads)
     psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
     seq = [[int(v) for v in window[c]] for c in range(omega)]   # post-burn-in samples (skip first psi)
 
@@ -287,6 +301,7 @@ def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: flo
     p = -(-eta // omega) * omega                    # line 6
     eta = kappa * p
     d = 0
+    trace = []
     # lines 7-12: randomness test on spaced batch means
     for _ in range(MAX_SKART_ITERS):
         ensure(eta // omega)
@@ -294,6 +309,7 @@ def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: flo
         bs = batch_sums(seq, 0, kappa, per) / kappa
         spaced = bs[:, ::d + 1]
         z = von_neumann_z(spaced)
+        trace.append((kappa, p, d, z, abs(z) <= z_pass))
         if abs(z) <= z_pass:
             break
         kappa = int(math.ceil(math.sqrt(2.0) * kappa))
@@ -308,7 +324,7 @@ def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: flo
         if ci.H <= h_star:
             return RunResult(estimate=ci.mu, rhat=rhat, psi=psi, steps_per_chain=ch.length,
                              gr_iterations=it, sample_size=eta, ci_lo=ci.ci_lo, ci_hi=ci.ci_hi,
-                             trace=[(kappa, p, d)])
+                             M=kappa, N=p, extensions=d, trace=trace + [("ci", kappa, p, d)])
         g = (ci.H / h_star) ** 2
         new_eta = int(math.ceil(g * eta))
         if p < P_CEILING:

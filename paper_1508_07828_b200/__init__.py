@@ -16,12 +16,14 @@ from .api import (  # noqa: F401
     pbn_load,
     pbn_validate,
     pbn_simulate,
+    pbn_simulate_workspace_size,
     pbn_recount,
     pbn_gelman_rubin,
     pbn_two_state,
     pbn_inv_norm_cdf,
     pbn_t_quantile,
     pbn_skart_ci_from_batches,
+    pbn_skart,
     pbn_run,
     pbn_run_multi,
     pbn_version,

@@ -65,7 +65,8 @@ class pbn_sim_args(C.Structure):
                 ("emit_bits", C.c_int32), ("bits_offset", C.c_int64), ("bits_row_words", C.c_int64),
                 ("groups_per_cta", C.c_int32), ("warps_per_group", C.c_int32),
                 ("schedule", C.c_int32), ("chunk_steps", C.c_int64), ("n_props", C.c_int32),
-                ("props", C.c_void_p), ("cluster_size", C.c_int32)]
+                ("props", C.c_void_p), ("cluster_size", C.c_int32), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_int64)]
 
 
 class pbn_sim_out(C.Structure):
@@ -82,6 +83,12 @@ class pbn_two_state_result(C.Structure):
 class pbn_skart_ci(C.Structure):
     _fields_ = [("mu", C.c_double), ("var", C.c_double), ("phi", C.c_double), ("skew", C.c_double),
                 ("ci_lo", C.c_double), ("ci_hi", C.c_double), ("H", C.c_double), ("batches", C.c_int64)]
+
+
+class pbn_skart_result(C.Structure):
+    _fields_ = [("estimate", C.c_double), ("ci_lo", C.c_double), ("ci_hi", C.c_double), ("H", C.c_double),
+                ("skew", C.c_double), ("kappa", C.c_int64), ("batches", C.c_int64), ("spacer", C.c_int64),
+                ("eta", C.c_int64), ("need_per_chain", C.c_int64), ("randomness_tests", C.c_int32)]
 
 
 class pbn_run_args(C.Structure):
@@ -112,6 +119,7 @@ SIGNATURES = {
     "pbn_free": (None, [C.c_void_p]),
     "pbn_get_model_info": (C.c_int, [C.c_void_p, C.POINTER(pbn_model_info)]),
     "pbn_simulate": (C.c_int, [C.c_void_p, C.POINTER(pbn_sim_args), C.POINTER(pbn_sim_out), C.c_void_p]),
+    "pbn_simulate_workspace_size": (C.c_int, [C.c_void_p, C.POINTER(pbn_sim_args), C.POINTER(C.c_int64)]),
     "pbn_recount": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                               C.c_void_p]),
@@ -124,6 +132,8 @@ SIGNATURES = {
     "pbn_t_quantile": (C.c_double, [C.c_double, C.c_double]),
     "pbn_skart_ci_from_batches": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                                             C.POINTER(pbn_skart_ci)]),
+    "pbn_skart": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                            C.POINTER(pbn_skart_result), C.c_void_p]),
     "pbn_run": (C.c_int, [C.c_void_p, C.POINTER(pbn_run_args), C.POINTER(pbn_run_result), C.c_void_p,
                           C.c_char_p, C.c_size_t]),
     "pbn_run_multi": (C.c_int, [C.c_void_p, C.POINTER(pbn_run_args), C.c_void_p, C.c_int32,

@@ -13,9 +13,10 @@ import numpy as np
 from . import _lib as L
 from ._lib import PbnError, check, lib
 
-__all__ = ["Model", "SimOutputs", "pbn_load", "pbn_validate", "pbn_simulate", "pbn_recount",
+__all__ = ["Model", "SimOutputs", "pbn_load", "pbn_validate", "pbn_simulate", "pbn_simulate_workspace_size",
+           "pbn_recount",
            "pbn_gelman_rubin", "pbn_two_state", "pbn_inv_norm_cdf", "pbn_t_quantile",
-           "pbn_skart_ci_from_batches", "pbn_run", "pbn_version", "alloc_outputs", "PbnError"]
+           "pbn_skart_ci_from_batches", "pbn_skart", "pbn_run", "pbn_version", "alloc_outputs", "PbnError"]
 
 
 def _desc(m, per_node: bool):
@@ -92,7 +93,9 @@ def pbn_load(model, per_node: bool = False, device: int = -1) -> Model:
 
 @dataclass
 class SimOutputs:
-    """Caller-owned device buffers (torch tensors), chain-major rows."""
+    """Caller-owned device buffers (torch tensors), chain-major rows, plus
+    the persistent-schedule scratch (`workspace`, sized by
+    pbn_simulate_workspace_size) so that pbn_simulate allocates nothing."""
     state: object
     c1: object = None
     n01: object = None
@@ -101,12 +104,20 @@ class SimOutputs:
     batch_sums: object = None
     bits: object = None
     totals: object = None
+    workspace: object = None
 
     def c_struct(self) -> L.pbn_sim_out:
         def p(t):
             return C.c_void_p(t.data_ptr()) if t is not None else None
         return L.pbn_sim_out(p(self.state), p(self.c1), p(self.n01), p(self.n10), p(self.first_last),
                              p(self.batch_sums), p(self.bits), p(self.totals))
+
+
+def pbn_simulate_workspace_size(model: Model, n_chains: int, n_props: int = 0) -> int:
+    a = L.pbn_sim_args(n_chains=int(n_chains), n_props=int(n_props))
+    b = C.c_int64()
+    check(lib().pbn_simulate_workspace_size(model.handle, C.byref(a), C.byref(b)))
+    return int(b.value)
 
 
 def alloc_outputs(model: Model, n_chains: int, steps: int, batch: int = 0, emit_bits: bool = False,
@@ -130,7 +141,65 @@ def alloc_outputs(model: Model, n_chains: int, steps: int, batch: int = 0, emit_
     if emit_bits:
         rw = bits_row_words or (steps + 31) // 32
         out.bits = torch.zeros(lead + (n_chains, rw), dtype=i32, device=dev)
+    ws = pbn_simulate_workspace_size(model, n_chains, n_props)
+    if ws > 0:
+        out.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
     return out
+
+
+def _check_outputs(model: Model, out: SimOutputs, *, n_chains: int, steps: int, batch: int, emit_bits: bool,
+                   bits_offset: int, bits_row_words: int, n_props: int) -> None:
+    """The C ABI writes through raw pointers: refuse tensors whose shape,
+    dtype, device or layout does not match the call (ValueError)."""
+    import torch
+    lead = (n_props,) if n_props > 0 else ()
+
+    def need(name, t, dtype, shape_ok, what):
+        if t is None:
+            return
+        if not isinstance(t, torch.Tensor):
+            raise ValueError(f"{name}: expected a torch tensor")
+        if t.dtype != dtype:
+            raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+        if t.device.type != "cuda":
+            raise ValueError(f"{name}: must be a CUDA tensor (got {t.device})")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
+        if not shape_ok(tuple(t.shape)):
+            raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {what}")
+
+    if out.state is None:
+        raise ValueError("state is required")
+    sw = model.state_words
+    need("state", out.state, torch.int32, lambda s: len(s) == 2 and s[0] >= n_chains and s[1] == sw,
+         f"(>= {n_chains}, {sw})")
+    # with several properties the blocks are strided by n_chains: exact rows
+    rows_ok = (lambda r: r == n_chains) if n_props > 0 else (lambda r: r >= n_chains)
+    for name, dt in [("c1", torch.int32), ("n01", torch.int32), ("n10", torch.int32),
+                     ("first_last", torch.uint8)]:
+        need(name, getattr(out, name), dt, lambda s: len(s) == len(lead) + 1 and s[:-1] == lead and rows_ok(s[-1]),
+             f"{lead} + (n_chains={n_chains},)")
+    need("totals", out.totals, torch.int64, lambda s: s == lead + (6,), f"{lead + (6,)}")
+    if steps > 0 and batch > 0:
+        nb = (steps + batch - 1) // batch
+        if out.batch_sums is None:
+            raise ValueError("batch > 0 needs batch_sums")
+        need("batch_sums", out.batch_sums, torch.int32,
+             lambda s: len(s) == len(lead) + 2 and s[:-2] == lead and rows_ok(s[-2]) and s[-1] == nb,
+             f"{lead} + (n_chains={n_chains}, {nb})")
+    if steps > 0 and emit_bits:
+        rw = bits_row_words or (steps + 31) // 32
+        if out.bits is None:
+            raise ValueError("emit_bits needs bits")
+        if rw < (bits_offset + steps + 31) // 32:
+            raise ValueError("bits_row_words too small for bits_offset + steps")
+        need("bits", out.bits, torch.int32,
+             lambda s: len(s) == len(lead) + 2 and s[:-2] == lead and rows_ok(s[-2]) and s[-1] == rw,
+             f"{lead} + (n_chains={n_chains}, {rw})")
+    if out.workspace is not None:
+        need("workspace", out.workspace, torch.uint8, lambda s: len(s) == 1, "(bytes,)")
+        if out.workspace.numel() < pbn_simulate_workspace_size(model, n_chains, n_props):
+            raise ValueError("workspace smaller than pbn_simulate_workspace_size()")
 
 
 def _pred(pred):
@@ -172,6 +241,11 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                        bits_row_words=bits_row_words, groups_per_cta=groups_per_cta,
                        warps_per_group=warps_per_group, schedule=schedule, chunk_steps=chunk_steps,
                        n_props=n_props, props=props_ptr, cluster_size=cluster_size)
+    _check_outputs(model, out, n_chains=n_chains, steps=steps, batch=batch, emit_bits=emit_bits,
+                   bits_offset=bits_offset, bits_row_words=bits_row_words, n_props=n_props)
+    if out.workspace is not None:
+        a.workspace = C.c_void_p(out.workspace.data_ptr())
+        a.workspace_bytes = out.workspace.numel()
     o = out.c_struct()
     check(lib().pbn_simulate(model.handle, C.byref(a), C.byref(o), _stream_handle(stream)))
     del keep_props  # the predicate arrays are read synchronously by the call above
@@ -216,6 +290,18 @@ def pbn_skart_ci_from_batches(batch_sums: np.ndarray, kappa: int, alpha_conf: fl
     res = L.pbn_skart_ci()
     st = lib().pbn_skart_ci_from_batches(bs.ctypes.data_as(C.c_void_p), omega, per, int(kappa),
                                          float(alpha_conf), C.byref(res))
+    return st, res
+
+
+def pbn_skart(bits, omega: int, row_words: int, start: int, available: int, h_star: float, alpha_conf: float,
+              stream=None):
+    """Skart sizing over device bitstreams (include/pbnsim.h pbn_skart).
+    Returns (status, pbn_skart_result): PBN_OK with the CI, or
+    PBN_E_NOT_CONVERGED with need_per_chain = samples per chain to simulate
+    before calling again."""
+    res = L.pbn_skart_result()
+    st = lib().pbn_skart(C.c_void_p(bits.data_ptr()), int(omega), int(row_words), int(start), int(available),
+                         float(h_star), float(alpha_conf), C.byref(res), _stream_handle(stream))
     return st, res
 
 

@@ -535,7 +535,6 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         return PBN_E_CUDA;
     const size_t limit = (size_t)smem_optin - 64;
     const int64_t groups = (a->n_chains + 31) / 32;
-    const bool k1_smem = (size_t)P.L.bytes + (size_t)P.group_words * 4 <= limit;
     auto fits = [&](const ClusterImages& ci) { return pbn::cluster_smem_bytes(P, ci.max_bytes) <= limit; };
     const ClusterImages* use = nullptr;
     if (a->cluster_size >= 2) {
@@ -582,7 +581,11 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         const size_t smem = pbn::cluster_smem_bytes(P, use->max_bytes);
         int active = 0;
         if (pbn::max_active_clusters(C, W, smem, &active) != 0 || active < 1) {
-            if (a->cluster_size >= 2 || !k1_smem) return PBN_E_USAGE;
+            // a forced cluster size must run as asked; in auto mode fall
+            // through to the one-CTA-per-group kernel (its image in shared
+            // memory or, when it does not fit, read through L1/L2)
+            cudaGetLastError();
+            if (a->cluster_size >= 2) return PBN_E_USAGE;
         } else {
             const int rc = pbn::launch_traj_cluster(C, W, smem, stream);
             return rc == 0 ? PBN_OK : PBN_E_CUDA;
@@ -594,8 +597,25 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     if (rc < 0) return PBN_E_USAGE;
     if (rc > 0) return PBN_E_CUDA;
     if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0) return PBN_E_USAGE;
-    rc = pbn::launch_traj(P, plan, m->device, a->schedule, a->chunk_steps, stream);
+    if (a->workspace_bytes < 0) return PBN_E_USAGE;
+    rc = pbn::launch_traj(P, plan, m->device, a->schedule, a->chunk_steps, a->workspace, (size_t)a->workspace_bytes,
+                          stream);
+    if (rc == -2) return PBN_E_USAGE;
     return rc == 0 ? PBN_OK : PBN_E_CUDA;
+}
+
+pbn_status pbn_simulate_workspace_size(pbn_model m, const pbn_sim_args* a, int64_t* bytes)
+{
+    if (!bytes) return PBN_E_USAGE;
+    *bytes = 0;
+    if (!m || !a || a->n_chains < 0 || a->n_props < 0 || a->n_props > PBN_MAX_PROPS) return PBN_E_USAGE;
+    pbn::TrajParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.n_chains = a->n_chains;
+    P.n_pad = (m->L.n + 3) & ~3;
+    P.n_props = a->n_props > 0 ? a->n_props : 1;
+    *bytes = a->n_chains > 0 ? (int64_t)pbn::traj_workspace_bytes(P) : 0;
+    return PBN_OK;
 }
 
 pbn_status pbn_recount(const uint32_t* bits, int64_t n_chains, int64_t row_words, int64_t start,

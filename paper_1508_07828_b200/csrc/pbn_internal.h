@@ -54,6 +54,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
+
+#include "../../include/pbnsim.h"
 
 namespace pbn {
 
@@ -165,8 +168,13 @@ struct LaunchPlan {
 // Implemented in pbn_traj.cu.  Returns 0 on success, a cudaError_t value on a
 // CUDA failure, or -1 (with *why set) when the sizes cannot be served.
 int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why);
-// schedule: 0 auto, 1 one CTA per 32-chain group, 2 persistent (chunk_steps 0 = auto)
-int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* stream);
+// schedule: 0 auto, 1 one CTA per 32-chain group, 2 persistent (chunk_steps 0 = auto).
+// workspace: caller-owned scratch of >= traj_workspace_bytes(P) bytes for the
+// persistent schedule, or NULL (one stream-ordered allocation per call).
+// Returns 0, a cudaError_t value, or -2 when the workspace is too small.
+size_t traj_workspace_bytes(const TrajParams& P);
+int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* workspace,
+                size_t workspace_bytes, void* stream);
 
 struct RecountParams {
     const uint32_t* bits;
@@ -179,5 +187,20 @@ struct RecountParams {
     unsigned long long* totals;
 };
 int launch_recount(const RecountParams& R, void* stream);
+
+// Pooled samples of omega chains for the Skart state machine (pbn_skart.cpp):
+// the count of ones among the first `len` samples of every chain, and the
+// chain-major sums of `per` consecutive kappa-batches of every chain from the
+// sample start ([omega x per], all chains -- gathered across shards).
+struct SkartSource {
+    virtual ~SkartSource() = default;
+    virtual pbn_status ones(int64_t len, uint64_t* S1) = 0;
+    virtual pbn_status batch_sums(int64_t kappa, int64_t per, std::vector<uint32_t>& out) = 0;
+};
+// Algorithm 5 lines 3-21 over the first `avail` samples per chain: PBN_OK
+// (res complete) or PBN_E_NOT_CONVERGED with res->need_per_chain > avail
+// (extend and call again; need_per_chain = 0: an iteration cap was hit).
+pbn_status skart_machine(SkartSource& src, int64_t omega, int64_t avail, double h_star, double alpha_conf,
+                         pbn_skart_result* res);
 
 }  // namespace pbn

@@ -172,6 +172,11 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
                 }
             }
         }
+        // a previous unit of this CTA (e.g. a ragged group, whose lanes
+        // without a chain may draw perturbations that never trigger the
+        // fix-up) can leave gamma bits behind: clear them per unit
+        if (!PER_NODE && P.persistent && it > 0)
+            for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
         const bool first_chunk = chunk == 0;
         const bool last_chunk = r_end >= total;
         // (kept in 32 bits: few live registers across the step loop -- the
@@ -499,7 +504,16 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
     return 0;
 }
 
-int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* stream)
+size_t traj_workspace_bytes(const TrajParams& P)
+{
+    const int64_t G = (P.n_chains + 31) / 32;
+    const int64_t stride = P.n_pad + 8 * 32 * (int64_t)std::max(P.n_props, 1);
+    const size_t ctl_bytes = ((8 + (size_t)G * 4) + 15) & ~(size_t)15;
+    return ctl_bytes + (size_t)G * (size_t)stride * 4 + 16;
+}
+
+int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* workspace,
+                size_t workspace_bytes, void* stream)
 {
     P.warps_per_group = plan.warps_per_group;
     P.node_warps = plan.node_warps;
@@ -528,6 +542,7 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
     P.persistent = persistent ? 1 : 0;
     int ctas = plan.ctas;
     uint8_t* ws = nullptr;
+    bool owned = false;
     if (persistent) {
         // ~128 units per CTA keeps the last round's imbalance below 1%; a unit
         // switch costs one group state save/restore (~10 KB through L2)
@@ -538,10 +553,18 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
         P.chunk_steps = K;
         P.total_units = G * ((total + K - 1) / K);
         P.scratch_stride = P.n_pad + 8 * 32 * (int64_t)std::max(P.n_props, 1);
-        const size_t scratch_bytes = (size_t)G * (size_t)P.scratch_stride * 4;
+        const size_t need = traj_workspace_bytes(P);
         const size_t ctl_bytes = 8 + (size_t)G * 4;
-        e = cudaMallocAsync(reinterpret_cast<void**>(&ws), scratch_bytes + ctl_bytes + 16, s);
-        if (e != cudaSuccess) return (int)e;
+        if (workspace) {
+            // caller-owned scratch (pbn_simulate_workspace_size): no allocation
+            if (workspace_bytes < need) return -2;
+            ws = reinterpret_cast<uint8_t*>(workspace);
+        } else {
+            // no workspace passed: one stream-ordered allocation for this call
+            e = cudaMallocAsync(reinterpret_cast<void**>(&ws), need, s);
+            if (e != cudaSuccess) return (int)e;
+            owned = true;
+        }
         P.work_ctr = reinterpret_cast<unsigned long long*>(ws);
         P.done = reinterpret_cast<uint32_t*>(ws + 8);
         P.scratch = reinterpret_cast<uint32_t*>(ws + ((ctl_bytes + 15) & ~(size_t)15));
@@ -551,7 +574,7 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
     }
     void* args[] = {&P};
     e = cudaLaunchKernel(fn, dim3(ctas), dim3(plan.threads), args, plan.smem_bytes, s);
-    if (ws) {
+    if (owned) {
         const cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;
     }

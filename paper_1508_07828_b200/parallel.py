@@ -63,13 +63,15 @@ def max_over_ranks(x: float, group=None) -> float:
 
 def run_sharded(model, *, omega: int, psi0: int, rhat_threshold: float = 1.1, r: float = 0.01,
                 s: float = 0.95, eps: float = 1e-10, seed: int = 0, pred=None, max_steps: int = 1 << 26,
-                group=None, stream=None):
-    """Algorithm 3 + Algorithm 4 over `omega` chains sharded across the ranks
-    of `group` (one GPU each): this rank simulates its contiguous block of
-    global chain ids and the pooled counts are summed with one all-reduce of
-    six u64 per decision (pbn_run_sharded, include/pbnsim.h).  Every rank
-    returns the same (status, pbn_run_result, err) as a single-GPU pbn_run
-    over all chains."""
+                method: int = 0, h_star: float = 1e-3, alpha_conf: float = 0.05, group=None, stream=None):
+    """Algorithm 3 + Algorithm 4 (method 0) or 5 (method 1, Skart) over
+    `omega` chains sharded across the ranks of `group` (one GPU each): this
+    rank simulates its contiguous block of global chain ids; pooled numbers
+    (six u64 counts per decision, or Skart's per-chain batch sums gathered
+    chain-major) are summed with one all-reduce (pbn_run_sharded,
+    include/pbnsim.h).  Every rank returns the same (status, pbn_run_result,
+    err) as a single-GPU pbn_run over all chains.  Needs omega >= world (every
+    rank simulates at least one chain)."""
     import ctypes as C
     import torch
     import torch.distributed as dist
@@ -77,6 +79,8 @@ def run_sharded(model, *, omega: int, psi0: int, rhat_threshold: float = 1.1, r:
     from .api import _pred, _stream_handle
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if omega < world:
+        raise ValueError(f"omega={omega} chains cannot be sharded over {world} ranks (each needs >= 1)")
     base, count = shard(omega, world, rank)
     nccl = dist.get_backend(group) == "nccl"
     state = {"error": None}
@@ -96,8 +100,8 @@ def run_sharded(model, *, omega: int, psi0: int, rhat_threshold: float = 1.1, r:
 
     cb = L.ALLREDUCE_FN(_allreduce)
     cp, _keep = _pred(pred)
-    a = L.pbn_run_args(method=0, omega=omega, psi0=psi0, rhat_threshold=rhat_threshold, r=r, s=s, eps=eps,
-                       seed=seed, pred=cp, max_steps=max_steps)
+    a = L.pbn_run_args(method=method, omega=omega, psi0=psi0, rhat_threshold=rhat_threshold, r=r, s=s, eps=eps,
+                       h_star=h_star, alpha_conf=alpha_conf, seed=seed, pred=cp, max_steps=max_steps)
     res = L.pbn_run_result()
     err = C.create_string_buffer(512)
     st = L.lib().pbn_run_sharded(model.handle, C.byref(a), base, count, C.cast(cb, C.c_void_p), None,
