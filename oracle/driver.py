@@ -45,6 +45,8 @@ class RunResult:
     beta: float = float("nan")
     ci_lo: float = float("nan")
     ci_hi: float = float("nan")
+    psi_gr: int = 0          # psi returned by Algorithm 3: the sample starts at state s_{psi_gr+1}
+    discarded: int = 0       # elements dropped at the front of every chain's sample (Alg 4 re-check)
     trace: list = field(default_factory=list)
 
 
@@ -99,9 +101,11 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
     discarded prefix is never shortened)."""
     ch = source if source is not None else Chains(model, pred, seed, omega, threads)
     psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
+    psi_gr = psi
     seq = [[int(v) for v in window[c]] for c in range(omega)]   # per-chain sample (GR window first)
     disc = 0                                         # elements discarded at the front
     ext_count = 0
+    trace = []
     while True:
         while True:
             L = max(len(seq[0]) - disc, 0)
@@ -121,6 +125,7 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
             ext_count += 1
         if ts.M > psi:
             disc += ts.M - psi
+            trace.append(("recheck", ts.M, psi, disc, len(seq[0])))
             psi = ts.M
             continue
         break
@@ -128,7 +133,7 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
     total_ones = sum(sum(x[disc:]) for x in seq)
     return RunResult(estimate=total_ones / (omega * L), rhat=rhat, psi=psi, steps_per_chain=ch.length,
                      gr_iterations=it, extensions=ext_count, sample_size=omega * L, M=ts.M, N=ts.N,
-                     alpha=ts.alpha, beta=ts.beta)
+                     alpha=ts.alpha, beta=ts.beta, psi_gr=psi_gr, discarded=disc, trace=trace)
 
 
 # --------------------------------------------------------------------------
@@ -324,7 +329,7 @@ def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: flo
         if ci.H <= h_star:
             return RunResult(estimate=ci.mu, rhat=rhat, psi=psi, steps_per_chain=ch.length,
                              gr_iterations=it, sample_size=eta, ci_lo=ci.ci_lo, ci_hi=ci.ci_hi,
-                             M=kappa, N=p, extensions=d, trace=trace + [("ci", kappa, p, d)])
+                             M=kappa, N=p, extensions=d, psi_gr=psi, trace=trace + [("ci", kappa, p, d)])
         g = (ci.H / h_star) ** 2
         new_eta = int(math.ceil(g * eta))
         if p < P_CEILING:

@@ -69,6 +69,14 @@ class SkartCI:
 PHI_CLAMP = 0.999999
 
 
+def skew_adjust(t: float, beta: float) -> float:
+    """Skewness adjustment of a t quantile: G(t) = (cbrt(1 + 6 beta
+    (t - beta)) - 1) / (2 beta), G(t) = t when beta = 0."""
+    if beta == 0.0:
+        return t
+    return float((np.cbrt(1 + 6 * beta * (t - beta)) - 1) / (2 * beta))
+
+
 def ci_from_batches(batch_sums: np.ndarray, kappa: int, alpha_conf: float) -> SkartCI:
     """Skewness- and autoregression-adjusted CI over chain-major
     batch means; lag-1 pairs never straddle chains (reading Q12)."""
@@ -79,7 +87,10 @@ def ci_from_batches(batch_sums: np.ndarray, kappa: int, alpha_conf: float) -> Sk
     mu = float(np.sum(Y)) / P
     dev = Y - mu
     ss = float(np.sum(dev ** 2))
-    if ss == 0.0:   # all batch means equal: zero-width interval
+    if ss == 0.0:
+        # all batch means equal: Var = 0, so the S:375 endpoints
+        # mu + G(t) sqrt(A Var / p') are both mu (skewness 0/0 undefined,
+        # reported as nan; the width does not depend on it)
         return SkartCI(mu, 0.0, 0.0, float("nan"), mu, mu, 0.0, P)
     var = ss / (P - 1)
     D = dev.reshape(omega, per)
@@ -89,16 +100,10 @@ def ci_from_batches(batch_sums: np.ndarray, kappa: int, alpha_conf: float) -> Sk
     skew = (float(np.sum(dev ** 3)) / P) / (ss / P) ** 1.5
     A = (1 + phi) / (1 - phi)
     beta = skew / (6.0 * math.sqrt(P))
-
-    def G(t):
-        if beta == 0.0:
-            return t
-        return (np.cbrt(1 + 6 * beta * (t - beta)) - 1) / (2 * beta)
-
     df = P - 1
     half = math.sqrt(A * var / P)
-    lo = mu + G(t_quantile(alpha_conf / 2, df)) * half
-    hi = mu + G(t_quantile(1 - alpha_conf / 2, df)) * half
+    lo = mu + skew_adjust(t_quantile(alpha_conf / 2, df), beta) * half
+    hi = mu + skew_adjust(t_quantile(1 - alpha_conf / 2, df), beta) * half
     return SkartCI(mu, var, phi, skew, float(lo), float(hi), float(max(mu - lo, hi - mu)), P)
 
 
