@@ -35,31 +35,73 @@ from workloads import CONFIGS, config_model, config_predicate  # noqa: E402
 METRIC = "PBN node-updates/sec and chain-steps/sec on 1 B200; fraction of int/smem roofline"
 UNIT = "node-updates/s"
 SM_COUNT_B200 = 148
-ALU_LANES_PER_CLK_PER_SM = 64   # ALU pipe: rt_SMSP = 2 cycles per warp-instruction (B300_MICROARCH.md)
 
 
-def algorithmic_alu_ops(model) -> float:
-    """ALU-pipe integer ops per node-update the method needs:
-    RNG 1/4 Philox4x32-10 = 5 LOP3 (the 5 IMAD.WIDE go to the FMA pipe);
-    decide 1 + (ell-1) compares; gather 2 per selected parent; lookup 2
-    (+1 word select when theta >= 6); commit 1."""
+def demand_per_node_update(model) -> dict:
+    """Algorithmic demand per node-update, SURVEY §8(d) (declared from the
+    method and the one-word-per-node-update stream of reading Q3, not from the
+    achieved SASS):
+      RNG     1/4 Philox4x32-10 = 5 IMAD.WIDE (FMA pipe) + 5 LOP3 (ALU)
+      decide  1 compare against T_p + (ell-1) compares/selects ~ ell + 1
+      gather  2 per parent of the selected function (extract + insert)
+      lookup  2 (+1 word select when the selected function has theta >= 6)
+      commit  1
+    smem: (theta_sel + 1)/32 wavefronts (one state word per selected parent
+    and one metadata read, each serving the 32 chains of a bit-sliced word).
+    theta_sel, [theta >= 6] are weighted by the selection probabilities."""
     ell = np.diff(model.fn_off).astype(np.float64)
     theta = np.diff(model.par_off).astype(np.float64)
-    # expected over the selected function: selection probabilities weight theta
     node_of_fn = np.repeat(np.arange(model.n), np.diff(model.fn_off))
-    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n)
-    sel_big = np.bincount(node_of_fn, weights=model.sel_prob * (theta >= 6), minlength=model.n)
-    return float(5.0 + ell.mean() + 2.0 * sel_theta.mean() + 2.0 + sel_big.mean() + 1.0)
+    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n).mean()
+    sel_big = np.bincount(node_of_fn, weights=model.sel_prob * (theta >= 6), minlength=model.n).mean()
+    alu = 5.0 + (ell.mean() + 1.0) + 2.0 * sel_theta + 2.0 + sel_big + 1.0
+    fma = 5.0
+    return {"alu": float(alu), "fma": fma, "issue": float(alu + fma), "lds_wavefronts": float((sel_theta + 1.0) / 32.0),
+            "theta_sel": float(sel_theta), "ell": float(ell.mean())}
 
 
-def algorithmic_smem_wavefronts(model) -> float:
-    """Shared-memory wavefronts per node-update the method needs with 32
-    chains bit-sliced per word: one state word per parent of the selected
-    function plus one metadata read, each serving 32 chains."""
-    theta = np.diff(model.par_off).astype(np.float64)
-    node_of_fn = np.repeat(np.arange(model.n), np.diff(model.fn_off))
-    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n)
-    return float((sel_theta.mean() + 1.0) / 32.0)
+def load_peaks() -> dict:
+    """Per-SM per-clock peaks measured by microbench/peaks.cu on a B200 of this
+    pool (profiles/peaks.json); the SM clock of the run scales them."""
+    path = os.path.join(ROOT, "profiles", "peaks.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            pk = json.load(f)
+        t = pk["tests"]
+        return {"source": "measured: profiles/peaks.json (microbench/peaks.cu, " + pk.get("when", "?") + ")",
+                "alu_warp_instr_per_clk": t["LOP3 (alu)"]["warp_instr_per_clk_per_sm"],
+                "fma_warp_instr_per_clk": t["IMAD (fma)"]["warp_instr_per_clk_per_sm"],
+                "issue_warp_instr_per_clk": t["LOP3+IMAD (issue)"]["warp_instr_per_clk_per_sm"],
+                "lds_wavefronts_per_clk": t["LDS.32 32 banks (1 wf)"]["warp_instr_per_clk_per_sm"],
+                "l2_read_gbs": pk.get("l2_read_gbs")}
+    # fallback: the guide's unit counts (B300_MICROARCH.md: ALU rt_SMSP = 2)
+    return {"source": "guide unit counts (no profiles/peaks.json)", "alu_warp_instr_per_clk": 2.0,
+            "fma_warp_instr_per_clk": 2.0, "issue_warp_instr_per_clk": 4.0, "lds_wavefronts_per_clk": 1.0,
+            "l2_read_gbs": None}
+
+
+def roofline(model, node_updates: float, kernel_s: float, sm_mhz: float) -> dict:
+    """Roofline of K1 in node-updates/s = min over resources of peak/demand
+    (SURVEY §8(d)); frac = achieved / roofline; `achieved`/`peak` are given
+    in the binding resource's unit (T ops/s or T wavefronts/s)."""
+    d = demand_per_node_update(model)
+    pk = load_peaks()
+    hz = sm_mhz * 1e6 * SM_COUNT_B200
+    res = {
+        "alu": (pk["alu_warp_instr_per_clk"] * 32 * hz, d["alu"], "Tops/s"),
+        "fma": (pk["fma_warp_instr_per_clk"] * 32 * hz, d["fma"], "Tops/s"),
+        "issue": (pk["issue_warp_instr_per_clk"] * 32 * hz, d["issue"], "Tinstr/s"),
+        "smem": (pk["lds_wavefronts_per_clk"] * hz, d["lds_wavefronts"], "Twavefronts/s"),
+    }
+    rate = node_updates / kernel_s
+    per = {k: {"peak": P / 1e12, "demand_per_node_update": D, "roofline_node_updates_per_s": P / D,
+               "frac": rate * D / P, "unit": U} for k, (P, D, U) in res.items()}
+    bound = min(per, key=lambda k: per[k]["roofline_node_updates_per_s"])
+    b = per[bound]
+    return {"bound": bound if bound != "smem" else "smem", "achieved": rate * b["demand_per_node_update"] / 1e12,
+            "peak": b["peak"], "unit": b["unit"], "frac": b["frac"],
+            "roofline_node_updates_per_s": b["roofline_node_updates_per_s"], "achieved_node_updates_per_s": rate,
+            "sm_mhz": sm_mhz, "peaks": pk, "per_resource": per, "demand": d}
 
 
 # --------------------------------------------------------------------------
@@ -199,9 +241,6 @@ def run_sweep(args, cfg, model, pred):
     import paper_1508_07828_b200 as pbn
     torch.cuda.set_device(0)
     pm = pbn.pbn_load(model)
-    ops = algorithmic_alu_ops(model)
-    smem_wf = algorithmic_smem_wavefronts(model)
-    peak = SM_COUNT_B200 * ALU_LANES_PER_CLK_PER_SM * 1965.0 * 1e6 / 1e12
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
     sweep = cfg.extra.get("chain_sweep", (1, 64, 1024, 16384))
@@ -226,10 +265,12 @@ def run_sweep(args, cfg, model, pred):
             ms.append(a.elapsed_time(b))
         t = statistics.median(ms) / 1e3
         nu = chains * (args.burn_in + args.window) * model.n
+        rf = roofline(model, nu, t, 1965.0)
         print(json.dumps({"sweep": cfg.key, "chains": chains, "n": model.n,
                           "steps_per_chain": args.burn_in + args.window,
                           "node_updates_per_s": nu / t, "chain_steps_per_s": chains * (args.burn_in + args.window) / t,
-                          "ms": t * 1e3, "roofline_frac_alu": nu * ops / t / 1e12 / peak,
+                          "ms": t * 1e3, "ms_best": min(ms) * 1.0, "roofline_frac": rf["frac"], "bound": rf["bound"],
+                          "roofline_node_updates_per_s": rf["roofline_node_updates_per_s"],
                           "image_bytes": int(pm.info.image_bytes)}), flush=True)
         del out
     pm.close()
@@ -253,6 +294,7 @@ def main():
     ap.add_argument("--schedule", type=int, default=0, help="0 auto, 1 CTA per group, 2 persistent")
     ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
     ap.add_argument("--sweep", action="store_true", help="C5 chain-count sweep (one line per count)")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="timed end-to-end (host buffer) iterations")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
@@ -336,16 +378,16 @@ def main():
 
     # ---- roofline of the dominant kernel (K1 traj_kernel; one launch per step) ----
     avg_kernel_s = statistics.mean(kern_ms) / 1e3
-    ops = algorithmic_alu_ops(model)
-    smem_wf = algorithmic_smem_wavefronts(model)
-    achieved = node_updates_per_step * ops / avg_kernel_s / 1e12       # T ALU-ops/s
-    sm_max = 1965.0
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            sm_max = float(json.load(f).get("sm_max_mhz", sm_max))
-    except Exception:
-        pass
-    peak = SM_COUNT_B200 * ALU_LANES_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    sm_mhz = None
+    if clk and clk.get("sm_mhz"):
+        sm_mhz = float(clk["sm_mhz"])           # SM clock sampled during the timed region
+    if not sm_mhz:
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                sm_mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+        except Exception:
+            sm_mhz = 1965.0
+    rf = roofline(model, node_updates_per_step, avg_kernel_s, sm_mhz)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_C4.json")
     if os.path.exists(tpath):
@@ -381,28 +423,39 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if dist:
-            ems = pbn.parallel.max_over_ranks(ems)
+        e2e_ms = []
+        for _ in range(max(1, args.e2e_steps)):
+            flush.fill_(7)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ems = e0.elapsed_time(e1)
+            if dist:
+                ems = pbn.parallel.max_over_ranks(ems)
+            e2e_ms.append(ems)
+        ems = statistics.median(e2e_ms)
         e2e = {"value": world * node_updates_per_step / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "pinned host state -> pbn_simulate -> all outputs to pinned host"}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": len(e2e_ms),
+               "ms_per_step_median": ems, "ms_per_step_best": min(e2e_ms),
+               "path": "pinned host state -> pbn_simulate -> all outputs to pinned host (median of steps)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = ncores()
         steps_s = 250_000 if model.n >= 1000 else 1_000_000  # ~10-20 s of oracle work
         v, info = oracle_sample(model, pred, cfg.sim_seed, cores, steps_s, cores)
+        # the same oracle on one core (one chain), a fifth of the per-chain steps
+        v1, info1 = oracle_sample(model, pred, cfg.sim_seed, 1, max(1, steps_s // 5), 1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{info['chains']} chains x {info['steps_per_chain']} transitions of "
                          f"{cfg.key} ({info['seconds']:.1f} s wall, one thread per chain)",
-               "per_core": v / cores, "cpu_model": cpu_model()}
+               "single_core": {"value": v1, "unit": UNIT, "cores": 1,
+                               "sample": f"1 chain x {info1['steps_per_chain']} transitions "
+                                         f"({info1['seconds']:.1f} s)"},
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -411,22 +464,17 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "chain_steps_per_s": chain_steps,
             "config": workload_config(args, cfg, model),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "ops_per_node_update": ops,
-                         "peak_basis": f"{SM_COUNT_B200} SMs x {ALU_LANES_PER_CLK_PER_SM} ALU lanes/clk "
-                                       f"x {sm_max:.0f} MHz (guide unit counts; sm_max_mhz of "
-                                       f"MEASURED_PEAKS.json)",
-                         "kernel": "traj_kernel (K1)", "kernel_ms": statistics.mean(kern_ms)},
-            # the secondary bound named by BASELINE's metric: shared-memory
-            # wavefronts, algorithmic demand (theta_sel + 1)/32 per node-update
-            # (metadata broadcast to 32 chains, one state word per selected
-            # parent), peak one wavefront per SM per clock
-            "roofline_smem": {"bound": "smem", "achieved": node_updates_per_step * smem_wf / avg_kernel_s / 1e12,
-                              "peak": SM_COUNT_B200 * sm_max * 1e6 / 1e12, "unit": "T wavefronts/s",
-                              "frac": (node_updates_per_step * smem_wf / avg_kernel_s)
-                              / (SM_COUNT_B200 * sm_max * 1e6),
-                              "wavefronts_per_node_update": smem_wf},
+            "roofline": {"bound": rf["bound"], "achieved": rf["achieved"], "peak": rf["peak"], "unit": rf["unit"],
+                         "frac": rf["frac"], "traffic": traffic,
+                         "roofline_node_updates_per_s": rf["roofline_node_updates_per_s"],
+                         "peak_basis": f"{rf['peaks']['source']}; x 32 lanes x {SM_COUNT_B200} SMs x "
+                                       f"{sm_mhz:.0f} MHz (SM clock sampled in the timed region); "
+                                       "roofline = min over resources of peak / demand (SURVEY 8(d))",
+                         "per_resource": rf["per_resource"], "demand": rf["demand"],
+                         "kernel": "traj_kernel (K1)", "kernel_ms_mean": statistics.mean(kern_ms),
+                         "kernel_ms_median": statistics.median(kern_ms), "kernel_ms_best": min(kern_ms)},
+            "value_best": node_updates_per_step * world / (min(kern_ms) / 1e3),
+            "value_median": node_updates_per_step * world / (statistics.median(kern_ms) / 1e3),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,

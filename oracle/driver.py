@@ -79,7 +79,8 @@ def generate_converged_chains(ch: Chains, psi0: int, threshold: float, max_steps
     it = 0
     while True:
         it += 1
-        g = ost.gelman_rubin_windows(window) if np.any(window.var(axis=1) > 0) else None
+        varying = np.any(window.min(axis=1) != window.max(axis=1))    # some window not constant
+        g = ost.gelman_rubin_windows(window) if varying else None
         rhat = g.rhat if g is not None else float("nan")
         if g is not None and rhat < threshold:
             return psi, rhat, it, window
@@ -102,14 +103,14 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
     ch = source if source is not None else Chains(model, pred, seed, omega, threads)
     psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
     psi_gr = psi
-    seq = [[int(v) for v in window[c]] for c in range(omega)]   # per-chain sample (GR window first)
+    seq = np.array(window, dtype=np.uint8)           # [omega x length] per-chain sample (GR window first)
     disc = 0                                         # elements discarded at the front
     ext_count = 0
     trace = []
     while True:
         while True:
-            L = max(len(seq[0]) - disc, 0)
-            counts = ost.estimate_alpha_beta([np.asarray(x[disc:]) for x in seq]) if L >= 2 else None
+            L = max(seq.shape[1] - disc, 0)
+            counts = ost.estimate_alpha_beta(list(seq[:, disc:])) if L >= 2 else None
             ts = ost.two_state(*counts, r, s, eps) if counts is not None else None
             if ts is not None and not ts.degenerate:
                 if ts.N <= omega * L:
@@ -120,17 +121,16 @@ def parallel_two_state(model, pred, seed: int, omega: int, psi0: int, threshold:
             if ch.length + ext > max_steps:
                 raise RuntimeError("two-state sample exceeds the step cap")
             I = ch.advance(0, ext)
-            for c in range(omega):
-                seq[c].extend(int(v) for v in I[c])
+            seq = np.concatenate([seq, np.asarray(I, np.uint8)], axis=1)
             ext_count += 1
         if ts.M > psi:
             disc += ts.M - psi
-            trace.append(("recheck", ts.M, psi, disc, len(seq[0])))
+            trace.append(("recheck", ts.M, psi, disc, seq.shape[1]))
             psi = ts.M
             continue
         break
-    L = len(seq[0]) - disc
-    total_ones = sum(sum(x[disc:]) for x in seq)
+    L = seq.shape[1] - disc
+    total_ones = int(seq[:, disc:].sum(dtype=np.int64))
     return RunResult(estimate=total_ones / (omega * L), rhat=rhat, psi=psi, steps_per_chain=ch.length,
                      gr_iterations=it, extensions=ext_count, sample_size=omega * L, M=ts.M, N=ts.N,
                      alpha=ts.alpha, beta=ts.beta, psi_gr=psi_gr, discarded=disc, trace=trace)
@@ -175,7 +175,7 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
         it += 1
         rh = []
         for w in windows:
-            if np.any(w.var(axis=1) > 0):
+            if np.any(w.min(axis=1) != w.max(axis=1)):
                 rh.append(ost.gelman_rubin_windows(w).rhat)
         if rh and all(x < threshold for x in rh):
             rhat = max(rh)
@@ -184,14 +184,14 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
             raise RuntimeError("Gelman-Rubin did not converge within the step cap")
         psi *= 2
         windows = [ch.advance(0, psi) for ch in chs]
-    seqs = [[[int(v) for v in w[c]] for c in range(omega)] for w in windows]
+    seqs = [np.array(w, dtype=np.uint8) for w in windows]      # per property [omega x length]
     disc, ext_count = 0, 0
     while True:
         while True:
-            L = max(len(seqs[0][0]) - disc, 0)
+            L = max(seqs[0].shape[1] - disc, 0)
             ts = []
             for p in range(q):
-                counts = ost.estimate_alpha_beta([np.asarray(x[disc:]) for x in seqs[p]]) if L >= 2 else None
+                counts = ost.estimate_alpha_beta(list(seqs[p][:, disc:])) if L >= 2 else None
                 t = ost.two_state(*counts, r, s, eps) if counts is not None else None
                 ts.append(t if (t is not None and not t.degenerate) else None)
             usable = [t for t in ts if t is not None]
@@ -206,8 +206,7 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
                 raise RuntimeError("two-state sample exceeds the step cap")
             for p in range(q):
                 I = chs[p].advance(0, ext)
-                for c in range(omega):
-                    seqs[p][c].extend(int(v) for v in I[c])
+                seqs[p] = np.concatenate([seqs[p], np.asarray(I, np.uint8)], axis=1)
             ext_count += 1
         Mmax = max([t.M for t in ts if t is not None], default=0)
         if Mmax > psi:
@@ -215,10 +214,10 @@ def parallel_two_state_multi(model, preds, seed: int, omega: int, psi0: int, thr
             psi = Mmax
             continue
         break
-    L = len(seqs[0][0]) - disc
+    L = seqs[0].shape[1] - disc
     per = []
     for p in range(q):
-        ones = sum(sum(x[disc:]) for x in seqs[p])
+        ones = int(seqs[p][:, disc:].sum(dtype=np.int64))
         t = ts[p]
         per.append({"estimate": ones / (omega * L), "degenerate": t is None,
                     "M": t.M if t else 0, "N": t.N if t else 0,
@@ -270,11 +269,12 @@ def von_neumann_z(means: np.ndarray) -> float:
     return (1.0 - Cst) * math.sqrt((m * m - 1.0) / (m - 2.0))
 
 
-def batch_sums(seq: list, start: int, kappa: int, per_chain: int) -> np.ndarray:
-    """Per-chain sums of per_chain consecutive kappa-batches from `start`."""
-    out = np.zeros((len(seq), per_chain), dtype=np.int64)
-    for c, x in enumerate(seq):
-        a = np.asarray(x[start:start + kappa * per_chain], dtype=np.int64)
+def batch_sums(seq: np.ndarray, start: int, kappa: int, per_chain: int) -> np.ndarray:
+    """Per-chain sums of per_chain consecutive kappa-batches from `start`
+    (seq: [omega x length] 0/1 samples)."""
+    out = np.zeros((seq.shape[0], per_chain), dtype=np.int64)
+    for c in range(seq.shape[0]):
+        a = np.asarray(seq[c, start:start + kappa * per_chain], dtype=np.int64)
         out[c] = a.reshape(per_chain, kappa).sum(axis=1)
     return out
 
@@ -286,21 +286,21 @@ def parallel_skart(model, pred, seed: int, omega: int, psi0: int, threshold: flo
     test, (kappa, p, d, z, passed) and finally ("ci", kappa, p, d)."""
     ch = source if source is not None else Chains(model, pred, seed, omega, threads)
     psi, rhat, it, window = generate_converged_chains(ch, psi0, threshold, max_steps)
-    seq = [[int(v) for v in window[c]] for c in range(omega)]   # post-burn-in samples (skip first psi)
+    seq = np.array(window, dtype=np.uint8)           # post-burn-in samples (skip first psi), [omega x length]
 
     def ensure(per_chain_len: int):
-        need = per_chain_len - len(seq[0])
+        nonlocal seq
+        need = per_chain_len - seq.shape[1]
         if need > 0:
             if ch.length + need > max_steps:
                 raise RuntimeError("Skart sample exceeds the step cap")
             I = ch.advance(0, need)
-            for c in range(omega):
-                seq[c].extend(int(v) for v in I[c])
+            seq = np.concatenate([seq, np.asarray(I, np.uint8)], axis=1)
 
     z_pass = ost.inv_norm_cdf(1.0 - RANDOMNESS_LEVEL / 2.0)
     eta = -(-1280 // omega) * omega                 # line 3
     ensure(eta // omega)
-    allx = np.concatenate([np.asarray(x[:eta // omega]) for x in seq])
+    allx = seq[:, :eta // omega].ravel()
     B = skewness(allx)                              # line 5, all samples
     kappa = 1 if (not math.isnan(B) and abs(B) <= SKEW_LIMIT) else 16
     p = -(-eta // omega) * omega                    # line 6

@@ -85,12 +85,15 @@ def _psrf_from_moments(mu_i: np.ndarray, s2_i: np.ndarray, psi: int) -> Psrf:
 
 def gelman_rubin_windows(windows: np.ndarray) -> Psrf:
     """windows: omega x psi array of the last psi values of each chain."""
-    X = np.asarray(windows, dtype=np.float64)
-    omega, psi = X.shape
+    omega, psi = np.shape(windows)
     if omega < 2 or psi < 2:
         raise ValueError("need omega >= 2 and psi >= 2")
-    mu_i = X.mean(axis=1)                                              # P:428
-    s2_i = ((X - mu_i[:, None]) ** 2).sum(axis=1) / (psi - 1)          # P:429 (divisor psi-1)
+    mu_i = np.zeros(omega)
+    s2_i = np.zeros(omega)
+    for i in range(omega):                   # one chain at a time (large windows stay small in memory)
+        x = np.asarray(windows[i], dtype=np.float64)
+        mu_i[i] = x.mean()                                             # P:428
+        s2_i[i] = ((x - mu_i[i]) ** 2).sum() / (psi - 1)               # P:429 (divisor psi-1)
     return _psrf_from_moments(mu_i, s2_i, psi)
 
 
@@ -154,13 +157,11 @@ def estimate_alpha_beta(seqs: list[np.ndarray]) -> tuple[int, int, int, int]:
     n01 = n0 = n10 = n1 = 0
     for s in seqs:
         s = np.asarray(s, dtype=np.int64)
-        for a, b in zip(s[:-1], s[1:]):
-            if a == 0:
-                n0 += 1
-                n01 += int(b == 1)
-            else:
-                n1 += 1
-                n10 += int(b == 0)
+        a, b = s[:-1], s[1:]                   # the pairs (I[t-1], I[t]) of this sequence
+        n0 += int(np.sum(a == 0))
+        n1 += int(np.sum(a == 1))
+        n01 += int(np.sum((a == 0) & (b == 1)))
+        n10 += int(np.sum((a == 1) & (b == 0)))
     return n01, n0, n10, n1
 
 

@@ -1,0 +1,9 @@
+# round-2 GPU pass: parity tests, smoke, measured peaks, bench (default C4)
+TAG=${1:-r2a}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 2400 python -m pytest tests -m gpu -q -rf --durations=15 > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu_$TAG.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_$TAG.log
+timeout 300 ./microbench/peaks > gpurun_out/peaks_$TAG.json 2> gpurun_out/peaks_$TAG.err; echo "peaks rc=$?"; cat gpurun_out/peaks_$TAG.json
+timeout 900 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/bench_$TAG.log | cut -c1-1500

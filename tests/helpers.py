@@ -91,3 +91,34 @@ def compare_chain(gpu: dict, row: int, st_packed: np.ndarray, ws, steps: int, ba
         assert np.array_equal(gpu["batch_sums"][row].astype(np.int64), ws.batch_sums), row
     if emit_bits and steps > 0:
         assert np.array_equal(gpu["bits"][row][:len(ws.bits)], ws.bits), row
+
+
+class GpuChains:
+    """Sample source for the oracle drivers (oracle/driver.py) backed by the
+    CUDA path: omega chains advanced with pbn_simulate (state carried between
+    calls, indicator bits read back).  Lets the oracle's own decision code run
+    on GPU trajectories at sizes the oracle simulator cannot reach (C3); the
+    trajectories themselves are pinned bit-exact to the oracle on sampled
+    chains by test_parity_gpu.py."""
+
+    def __init__(self, pbn, pm, pred, seed: int, omega: int, chain_base: int = 0):
+        self.pbn, self.pm, self.pred, self.seed = pbn, pm, pred, seed
+        self.omega, self.chain_base = omega, chain_base
+        self.length = 0
+        self.state = None
+
+    def advance(self, burn_in: int, steps: int) -> np.ndarray:
+        import torch
+        out = self.pbn.alloc_outputs(self.pm, self.omega, steps, emit_bits=True)
+        if self.state is not None:
+            out.state.copy_(self.state)
+        self.pbn.pbn_simulate(self.pm, out, n_chains=self.omega, chain_base=self.chain_base, steps=steps,
+                              step0=self.length, burn_in=burn_in, seed=self.seed, pred=self.pred,
+                              init=self.state is None, emit_bits=True)
+        torch.cuda.synchronize()
+        self.state = out.state.clone()
+        self.length += burn_in + steps
+        if steps == 0:
+            return np.zeros((self.omega, 0), np.uint8)
+        bits = np.ascontiguousarray(out.bits.cpu().numpy().view(np.uint32))
+        return np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")[:, :steps]

@@ -65,6 +65,21 @@ def test_two_state_driver_burn_in_recheck(pbn):
     check_two_state(res, o)
 
 
+def test_two_state_driver_burn_in_discard_past_the_sample(pbn):
+    """a burn-in re-check whose M - psi exceeds the current sample
+    (identity network, alpha = beta = p = 1e-3, omega = 16, r = 0.1): the
+    discard continues into the next extension, in the library
+    driver exactly as in the oracle's (pinned by re-simulation in
+    test_oracle_driver_pins.py)."""
+    from workloads import model_from_lists
+    model = model_from_lists(1, 0.001, [[([0], [0, 1], 1.0)]])
+    pred = Predicate(np.array([0], np.uint16), np.array([1], np.uint8))
+    res, o = run_both_two_state(pbn, model, pred, omega=16, psi0=8, thr=1.1, r=0.1, s=0.95, eps=1e-10, seed=3,
+                                max_steps=1 << 24)
+    assert any(t[3] > t[4] for t in o.trace)
+    check_two_state(res, o)
+
+
 def test_two_state_driver_C2_config(pbn):
     """BASELINE C2: 1024 chains, psi0 = 1000, R-hat < 1.1, r = 0.01, s = 0.95."""
     c = CONFIGS["C2"]
@@ -84,10 +99,9 @@ def test_skart_driver(pbn, omega, seed):
                                alpha_conf=0.05, seed=seed, pred=pred, max_steps=1 << 22)
     assert st == 0, err
     o = odr.parallel_skart(model, pred, seed, omega, 256, 1.1, 0.01, 0.05, 1 << 22, threads=16)
-    kappa, p, d = o.trace[-1]
     assert (res.psi, res.gr_iterations, res.sample_size, res.steps_per_chain) == (
         o.psi, o.gr_iterations, o.sample_size, o.steps_per_chain)
-    assert (res.M, res.N) == (kappa, p)
+    assert (res.M, res.N, res.extensions) == (o.M, o.N, o.extensions)     # kappa, p, spacer d
     for a, b in [(res.estimate, o.estimate), (res.ci_lo, o.ci_lo), (res.ci_hi, o.ci_hi), (res.rhat, o.rhat)]:
         assert close(a, b), (a, b)
     assert res.ci_lo <= res.estimate <= res.ci_hi
@@ -170,5 +184,109 @@ def test_sharded_driver_equals_single_gpu_run(pbn):
     assert st == 0, err
     ref = np.array([st, res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain,
                     res.M, res.N, res.estimate, res.rhat, res.alpha, res.beta], dtype=np.float64)
+    for g in got:
+        assert np.array_equal(g, ref), (g, ref)
+
+
+def test_skart_driver_C3_protocol(pbn):
+    """BASELINE C3 (n = 1000, 4096 chains, Gelman-Rubin from psi0 = 5e4, i.e.
+    10^5 transitions per chain, then Skart, H* = 1e-3, alpha = 0.05) end to
+    end through pbn_run(SKART), against the oracle's Algorithm 3 + 5 decision
+    code (oracle/driver.py) run on the same GPU trajectories (tests.helpers
+    .GpuChains; the trajectories are bit-exact to the oracle simulator on 64
+    sampled chains in test_parity_gpu.py): identical psi, kappa, p, spacer
+    and steps, estimate / CI / R-hat within 1e-9."""
+    from tests.helpers import GpuChains
+    c = CONFIGS["C3"]
+    model, pred = config_model("C3"), config_predicate("C3")
+    pm = pbn.pbn_load(model)
+    kw = dict(omega=c.chains, psi0=c.burn_in, rhat_threshold=1.1, h_star=1e-3, alpha_conf=0.05, seed=c.sim_seed,
+              pred=pred, max_steps=1 << 22)
+    st, res, err = pbn.pbn_run(pm, method=1, **kw)
+    assert st == 0, err
+    src = GpuChains(pbn, pm, pred, c.sim_seed, c.chains)
+    o = odr.parallel_skart(model, pred, c.sim_seed, c.chains, c.burn_in, 1.1, 1e-3, 0.05, 1 << 22, source=src)
+    assert (res.psi, res.gr_iterations, res.sample_size, res.steps_per_chain) == (
+        o.psi, o.gr_iterations, o.sample_size, o.steps_per_chain)
+    assert (res.M, res.N, res.extensions) == (o.M, o.N, o.extensions)
+    for a, b in [(res.estimate, o.estimate), (res.ci_lo, o.ci_lo), (res.ci_hi, o.ci_hi), (res.rhat, o.rhat)]:
+        assert close(a, b), (a, b)
+
+
+@pytest.mark.parametrize("omega,seed", [(8, 3), (5, 11)])
+def test_pbn_skart_boundary_call(pbn, omega, seed):
+    """pbn_skart (C ABI) over device bitstreams, called with a growing
+    sample until it stops asking for more, against the oracle's Algorithm 5
+    decisions on the same trajectories."""
+    import torch
+    from tests.helpers import GpuChains
+    model = random_pbn(12, 1, 3, 1, 3, 0.02, seed=seed)
+    pred = Predicate(np.array([0, 5], np.uint16), np.array([1, 0], np.uint8))
+    pm = pbn.pbn_load(model)
+    o = odr.parallel_skart(model, pred, seed, omega, 256, 1.1, 0.01, 0.05, 1 << 22,
+                           source=GpuChains(pbn, pm, pred, seed, omega))
+    psi = o.psi
+    # the chains after Algorithm 3: 2 psi transitions, sample = the last psi
+    avail, calls = psi, 0
+    while True:
+        total = psi + avail
+        out = pbn.alloc_outputs(pm, omega, total, emit_bits=True)
+        pbn.pbn_simulate(pm, out, n_chains=omega, steps=total, seed=seed, pred=pred, init=True, emit_bits=True)
+        torch.cuda.synchronize()
+        st, r = pbn.pbn_skart(out.bits, omega, out.bits.shape[1], psi, avail, 0.01, 0.05)
+        calls += 1
+        if st == 0:
+            break
+        assert st == 4 and r.need_per_chain > avail, (st, r.need_per_chain)
+        avail = r.need_per_chain
+    assert psi + avail == o.steps_per_chain
+    assert (r.kappa, r.batches, r.spacer, r.eta) == (o.M, o.N, o.extensions, o.sample_size)
+    for a, b in [(r.estimate, o.estimate), (r.ci_lo, o.ci_lo), (r.ci_hi, o.ci_hi)]:
+        assert close(a, b), (a, b)
+
+
+def _sharded_skart_rank(rank, world, port, outdir):
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_1508_07828_b200 as pbn
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    model = random_pbn(12, 1, 3, 1, 3, 0.02, seed=3)
+    pred = Predicate(np.array([0, 5], np.uint16), np.array([1, 0], np.uint8))
+    pm = pbn.pbn_load(model)
+    st, res, err = pbn.parallel.run_sharded(pm, omega=9, psi0=256, rhat_threshold=1.1, seed=3, pred=pred,
+                                            method=1, h_star=0.01, alpha_conf=0.05, max_steps=1 << 22)
+    np.save(os.path.join(outdir, f"r{rank}.npy"),
+            np.array([st, res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain,
+                      res.M, res.N, res.estimate, res.rhat, res.ci_lo, res.ci_hi], dtype=np.float64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_skart_equals_single_gpu_run(pbn):
+    """Skart over chains sharded on 2 ranks (9 chains: 5 + 4; per-chain batch
+    sums all-gathered, Fig. 2b) gives the single-GPU pbn_run's decisions and
+    CI bit for bit."""
+    import socket
+    import tempfile
+    import torch.multiprocessing as mp
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_sharded_skart_rank, args=(2, port, d), nprocs=2, join=True)
+        got = [np.load(f"{d}/r{r}.npy") for r in range(2)]
+    model = random_pbn(12, 1, 3, 1, 3, 0.02, seed=3)
+    pred = Predicate(np.array([0, 5], np.uint16), np.array([1, 0], np.uint8))
+    pm = pbn.pbn_load(model)
+    st, res, err = pbn.pbn_run(pm, method=1, omega=9, psi0=256, rhat_threshold=1.1, h_star=0.01, alpha_conf=0.05,
+                               seed=3, pred=pred, max_steps=1 << 22)
+    assert st == 0, err
+    ref = np.array([st, res.psi, res.gr_iterations, res.extensions, res.sample_size, res.steps_per_chain,
+                    res.M, res.N, res.estimate, res.rhat, res.ci_lo, res.ci_hi], dtype=np.float64)
     for g in got:
         assert np.array_equal(g, ref), (g, ref)

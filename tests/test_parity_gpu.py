@@ -7,6 +7,8 @@ Small configs are compared on all chains; C3-C5 run in the exact launch
 configuration bench.py times and are compared on a deterministic sample of
 chains that the oracle computes one by one at the full step count.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -32,10 +34,10 @@ def load(pbn, model, per_node=False):
 
 
 def full_compare(pbn, model, pred, *, n_chains, steps, burn_in=0, seed=1, batch=0, per_node=False,
-                 groups=0, warps=0, threads=8):
+                 groups=0, warps=0, threads=8, cluster_size=0):
     pm = load(pbn, model, per_node)
     g = gpu_run(pm, model, pred, n_chains=n_chains, steps=steps, burn_in=burn_in, seed=seed,
-                batch=batch, groups=groups, warps=warps)
+                batch=batch, groups=groups, warps=warps, cluster_size=cluster_size)
     st, I, ws = oracle_run(model, pred, np.arange(n_chains), steps=steps, burn_in=burn_in, seed=seed,
                            batch=batch, per_node=per_node, threads=threads)
     packed = pack_states(st)
@@ -63,19 +65,24 @@ def test_C2_all_chains(pbn):
                  burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch)
 
 
-@pytest.mark.parametrize("key", ["C3", "C4", "C5"])
-def test_large_configs_sampled_chains(pbn, key):
-    """Full launch (bench.py's configuration); oracle on sampled chains."""
+@pytest.mark.parametrize("key,n_chains", [("C3", 0), ("C4", 0), ("C5", 1), ("C5", 64), ("C5", 1024), ("C5", 16384),
+                                          ("C5", 65536)])
+def test_large_configs_sampled_chains(pbn, key, n_chains):
+    """Full launch in the configuration bench.py times (C3, C4; C5 at every
+    chain count of its sweep, with the kernel pbn_simulate auto-selects
+    there: clusters of 16 / 8 CTAs for 1-1024 chains, the global-image K1
+    beyond); the oracle recomputes up to 64 sampled chains at the full step
+    count; invariants on every chain."""
     c = CONFIGS[key]
     model, pred = config_model(key), config_predicate(key)
-    n_chains = c.chains
+    n_chains = n_chains or c.chains
     steps, burn_in = c.steps, c.burn_in
     pm = load(pbn, model)
     g = gpu_run(pm, model, pred, n_chains=n_chains, steps=steps, burn_in=burn_in, seed=c.sim_seed,
                 batch=c.batch)
-    ids = sample_chain_ids(n_chains, k=8, seed=c.sim_seed)
+    ids = sample_chain_ids(n_chains, k=64, seed=c.sim_seed)
     st, I, ws = oracle_run(model, pred, ids, steps=steps, burn_in=burn_in, seed=c.sim_seed,
-                           batch=c.batch, threads=8)
+                           batch=c.batch, threads=os.cpu_count() or 8)
     packed = pack_states(st)
     for k, cid in enumerate(ids):
         compare_chain(g, cid, packed[k], ws[k], steps, c.batch)
@@ -93,21 +100,56 @@ def test_large_configs_sampled_chains(pbn, key):
     assert tot[5] == int((c1 - last).sum()) and tot[4] == int(((steps - c1) - (1 - last)).sum())
 
 
-def test_launch_shape_independence(pbn):
+ALL = ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]
+
+
+@pytest.mark.parametrize("per_node", [False, True])
+def test_launch_shape_independence(pbn, per_node):
+    """cluster_size=1 forces the single-CTA kernel K1 (200 chains = 7 groups
+    would otherwise auto-select the cluster kernel): K1's warp splits and
+    its persistent chunking are compared with K1 one-CTA-per-group, and the
+    auto (cluster) launch with both; the oracle checks the reference."""
     model, pred = config_model("C2"), config_predicate("C2")
-    pm = load(pbn, model)
-    ref = gpu_run(pm, model, pred, n_chains=200, steps=700, burn_in=300, seed=9, batch=64)
+    pm = load(pbn, model, per_node)
+    kw = dict(n_chains=200, steps=700, burn_in=300, seed=9, batch=64)
+    ref = gpu_run(pm, model, pred, cluster_size=1, schedule=1, **kw)
+    auto = gpu_run(pm, model, pred, **kw)
+    for k in ALL:
+        assert np.array_equal(auto[k], ref[k]), ("auto", k)
     for warps in [1, 2, 5, 7, 8, 13, 25]:
-        g = gpu_run(pm, model, pred, n_chains=200, steps=700, burn_in=300, seed=9, batch=64,
-                    warps=warps)
-        for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]:
+        g = gpu_run(pm, model, pred, warps=warps, cluster_size=1, schedule=1, **kw)
+        for k in ALL:
             assert np.array_equal(g[k], ref[k]), (warps, k)
     # persistent schedule: chunks straddle the burn-in end, batch and bit-word boundaries
     for chunk, warps in [(1, 4), (7, 25), (33, 3), (299, 0), (1000, 8), (0, 0)]:
-        g = gpu_run(pm, model, pred, n_chains=200, steps=700, burn_in=300, seed=9, batch=64,
-                    warps=warps, schedule=2, chunk_steps=chunk)
-        for k in ["state", "c1", "n01", "n10", "first_last", "batch_sums", "bits", "totals"]:
+        g = gpu_run(pm, model, pred, warps=warps, schedule=2, chunk_steps=chunk, cluster_size=1, **kw)
+        for k in ALL:
             assert np.array_equal(g[k], ref[k]), ("persistent", chunk, warps, k)
+    ids = sample_chain_ids(200, k=6, seed=9)
+    st, I, ws = oracle_run(model, pred, ids, steps=700, burn_in=300, seed=9, batch=64, per_node=per_node)
+    packed = pack_states(st)
+    for j, cid in enumerate(ids):
+        compare_chain(ref, cid, packed[j], ws[j], 700, 64)
+
+
+@pytest.mark.parametrize("per_node", [False, True])
+def test_persistent_ragged_group_leaves_no_gamma_bits(pbn, per_node):
+    """a ragged last group (20007 chains: 7 real lanes in group
+    625) whose chain-less lanes draw perturbations must not leak gamma bits
+    into the next work unit of the same CTA (persistent schedule, short
+    chunks so every CTA runs many units)."""
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = load(pbn, model, per_node)
+    kw = dict(n_chains=20007, steps=300, burn_in=60, seed=4, batch=50, cluster_size=1)
+    a = gpu_run(pm, model, pred, schedule=1, **kw)
+    b = gpu_run(pm, model, pred, schedule=2, chunk_steps=13, **kw)
+    for k in ALL:
+        assert np.array_equal(a[k], b[k]), k
+    ids = [0, 19999, 20000, 20006] + sample_chain_ids(20007, k=4, seed=2)
+    st, I, ws = oracle_run(model, pred, ids, steps=300, burn_in=60, seed=4, batch=50, per_node=per_node)
+    packed = pack_states(st)
+    for j, cid in enumerate(ids):
+        compare_chain(b, cid, packed[j], ws[j], 300, 50)
 
 
 def test_persistent_schedule_large_group_count(pbn):
@@ -127,19 +169,21 @@ def test_persistent_schedule_large_group_count(pbn):
             compare_chain(b, cid, packed[j], ws[j], 150, 16)
 
 
-def test_chain_split_and_step_split(pbn):
+@pytest.mark.parametrize("cluster_size", [1, 0])
+def test_chain_split_and_step_split(pbn, cluster_size):
     model, pred = config_model("C2"), config_predicate("C2")
     pm = load(pbn, model)
-    full = gpu_run(pm, model, pred, n_chains=100, steps=640, burn_in=0, seed=5, batch=0)
+    cs = dict(cluster_size=cluster_size)
+    full = gpu_run(pm, model, pred, n_chains=100, steps=640, burn_in=0, seed=5, batch=0, **cs)
     # chains 0..36 and 37..99 in separate calls (chain_base)
-    a = gpu_run(pm, model, pred, n_chains=37, steps=640, seed=5)
-    b = gpu_run(pm, model, pred, n_chains=63, chain_base=37, steps=640, seed=5)
+    a = gpu_run(pm, model, pred, n_chains=37, steps=640, seed=5, **cs)
+    b = gpu_run(pm, model, pred, n_chains=63, chain_base=37, steps=640, seed=5, **cs)
     for k in ["state", "c1", "n01", "n10", "first_last", "bits"]:
         assert np.array_equal(np.concatenate([a[k], b[k]]), full[k]), k
     # steps 0..300 then 301..640 continuing the state; bits appended at an offset
-    s1 = gpu_run(pm, model, pred, n_chains=100, steps=300, seed=5, bits_row_words=20)
+    s1 = gpu_run(pm, model, pred, n_chains=100, steps=300, seed=5, bits_row_words=20, **cs)
     s2 = gpu_run(pm, model, pred, n_chains=100, steps=340, step0=300, seed=5, init=False,
-                 state=s1["state"], bits_offset=300, bits_row_words=20, bits_init=s1["bits"])
+                 state=s1["state"], bits_offset=300, bits_row_words=20, bits_init=s1["bits"], **cs)
     assert np.array_equal(s2["state"], full["state"])
     assert np.array_equal(s2["bits"][:, :20], full["bits"][:, :20])
     assert np.array_equal(s1["c1"].astype(np.int64) + s2["c1"], full["c1"])
@@ -171,11 +215,15 @@ def edge_models():
         np.array([0], np.uint16), np.array([1], np.uint8))
 
 
+@pytest.mark.parametrize("cluster_size", [1, 0])
 @pytest.mark.parametrize("per_node", [False, True])
 @pytest.mark.parametrize("name,model,pred", list(edge_models()), ids=[e[0] for e in edge_models()])
-def test_edge_models(pbn, name, model, pred, per_node):
+def test_edge_models(pbn, name, model, pred, per_node, cluster_size):
+    """cluster_size=1: the single-CTA kernel K1 with the image in shared
+    memory (FT = 3..8 and the generic path); 0: auto (45 chains = 2 groups
+    -> the cluster kernel wherever the model has enough quads)."""
     full_compare(pbn, model, pred, n_chains=45, steps=777, burn_in=123, seed=17, batch=50,
-                 per_node=per_node)
+                 per_node=per_node, cluster_size=cluster_size)
 
 
 def test_edge_sizes(pbn):
