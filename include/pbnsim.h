@@ -144,6 +144,9 @@ typedef struct {
  *                between chunks in `workspace`
  *   chunk_steps  persistent chunk length (0 = auto)
  *   workspace    caller-owned device scratch (see pbn_simulate_workspace_size)
+ *   layout       PBN_LAYOUT_*: chains over the lanes of a warp (K1 / K1c) or,
+ *                for few chains, nodes over the threads of a cluster (K1n)
+ *   chains_per_cluster  K1n: chains sharing one cluster (0 = auto)
  *   cluster_size 0: chosen per call -- one CTA per 32-chain group when the
  *                device image fits one CTA's shared memory and there are
  *                enough groups to fill the GPU, else a thread-block cluster of
@@ -177,7 +180,17 @@ typedef struct {
                                     /* cluster of that many CTAs per group         */
     void* workspace;                /* caller-owned DEVICE scratch of at least     */
     int64_t workspace_bytes;        /* pbn_simulate_workspace_size() bytes, or NULL */
+    int32_t layout;                 /* PBN_LAYOUT_*: which lanes a warp spreads    */
+    int32_t chains_per_cluster;     /* NODE_LANES: chains per cluster, 1..32 (0 = auto) */
 } pbn_sim_args;
+
+/* Kernel layouts (pbn_sim_args.layout).  Outputs never depend on it. */
+enum {
+    PBN_LAYOUT_AUTO = 0,        /* chosen per call from the chain count and image size  */
+    PBN_LAYOUT_CHAIN_LANES = 1, /* 32 chains per warp, bit-sliced state (K1, K1c)       */
+    PBN_LAYOUT_NODE_LANES = 2   /* one chain per cluster of cluster_size CTAs (0 = auto), */
+                                /* threads over node quads, bit-packed state (K1n)     */
+};
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).
  *   state       [n_chains x ceil(n/32)] u32, in/out; node i of chain c is

@@ -7,8 +7,9 @@
 // barrier and over-reported): every kernel runs 2 CTAs x 1024
 // threads on every SM; each CTA brackets its timed loop with __syncthreads()
 // and records clock64() and %globaltimer at both ends (thread 0), so
-//   rate   = warp-instructions issued by the CTA pair / the SM's cycle count
-//            (the max over its two CTAs of the barrier-bracketed window)
+//   rate   = warp-instructions issued by the SM's CTAs / the SM's cycle count
+//            over the union of their barrier-bracketed windows (clock64 is
+//            the SM's own counter)
 //   clock  = cycles / globaltimer ns of the same window (the SM clock under
 //            this load, MHz)
 // and the whole grid is also timed with CUDA events (elapsed_ms).  One
@@ -20,9 +21,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 
-#define ITERS 8192
+#define ITERS 32768
 #define CHECK(x)                                                                       \
     do {                                                                               \
         cudaError_t e_ = (x);                                                          \
@@ -32,8 +34,8 @@
         }                                                                              \
     } while (0)
 
-__device__ unsigned long long g_cycles[4096];
-__device__ unsigned long long g_ns[4096];
+__device__ unsigned long long g_c0[4096], g_c1[4096];  // clock64 at the window ends (per-SM counter)
+__device__ unsigned long long g_n0[4096], g_n1[4096];  // %globaltimer at the window ends
 __device__ uint32_t g_smid[4096];
 __device__ uint32_t g_sink[1 << 20];
 
@@ -120,8 +122,10 @@ __global__ void __launch_bounds__(1024, 2) kbench(uint32_t seed)
     }
     __syncthreads();
     if (tid == 0) {
-        g_cycles[blockIdx.x] = clock64() - t0;
-        g_ns[blockIdx.x] = gtimer() - n0;
+        g_c0[blockIdx.x] = t0;
+        g_c1[blockIdx.x] = clock64();
+        g_n0[blockIdx.x] = n0;
+        g_n1[blockIdx.x] = gtimer();
         g_smid[blockIdx.x] = smid();
     }
     uint32_t acc = 0;
@@ -166,26 +170,31 @@ Res run(int sms)
     CHECK(cudaDeviceSynchronize());
     float ms = 0;
     CHECK(cudaEventElapsedTime(&ms, a, b));
-    std::vector<unsigned long long> cyc(blocks), ns(blocks);
+    std::vector<unsigned long long> c0(blocks), c1(blocks), n0(blocks), n1(blocks);
     std::vector<uint32_t> sid(blocks);
-    CHECK(cudaMemcpyFromSymbol(cyc.data(), g_cycles, sizeof(unsigned long long) * blocks));
-    CHECK(cudaMemcpyFromSymbol(ns.data(), g_ns, sizeof(unsigned long long) * blocks));
+    CHECK(cudaMemcpyFromSymbol(c0.data(), g_c0, sizeof(unsigned long long) * blocks));
+    CHECK(cudaMemcpyFromSymbol(c1.data(), g_c1, sizeof(unsigned long long) * blocks));
+    CHECK(cudaMemcpyFromSymbol(n0.data(), g_n0, sizeof(unsigned long long) * blocks));
+    CHECK(cudaMemcpyFromSymbol(n1.data(), g_n1, sizeof(unsigned long long) * blocks));
     CHECK(cudaMemcpyFromSymbol(sid.data(), g_smid, sizeof(uint32_t) * blocks));
-    // per SM: the CTAs it ran (2, co-resident), window = max of their windows
-    std::vector<unsigned long long> smc(4096, 0), smn(4096, 0);
+    // per SM: the UNION of the windows of the CTAs it ran (clock64 is the
+    // SM's own cycle counter, so the windows of co-resident CTAs compare)
+    std::vector<unsigned long long> lo(4096, ~0ull), hi(4096, 0), nlo(4096, ~0ull), nhi(4096, 0);
     std::vector<int> cnt(4096, 0);
     for (int i = 0; i < blocks; ++i) {
         const uint32_t s = sid[i] & 4095u;
-        if (cyc[i] > smc[s]) smc[s] = cyc[i];
-        if (ns[i] > smn[s]) smn[s] = ns[i];
+        lo[s] = std::min(lo[s], c0[i]);
+        hi[s] = std::max(hi[s], c1[i]);
+        nlo[s] = std::min(nlo[s], n0[i]);
+        nhi[s] = std::max(nhi[s], n1[i]);
         cnt[s]++;
     }
     double rate = 0, mhz = 0;
     int used = 0;
     for (int s = 0; s < 4096; ++s)
         if (cnt[s]) {
-            rate += (double)cnt[s] * 32.0 * ITERS / (double)smc[s];
-            mhz += (double)smc[s] / (double)smn[s] * 1e3;
+            rate += (double)cnt[s] * 32.0 * ITERS / (double)(hi[s] - lo[s]);
+            mhz += (double)(hi[s] - lo[s]) / (double)(nhi[s] - nlo[s]) * 1e3;
             used++;
         }
     Res r;

@@ -31,6 +31,9 @@ STATUS_NAMES = {0: "PBN_OK", 1: "PBN_E_INVALID", 2: "PBN_E_USAGE", 3: "PBN_E_DEG
 
 PBN_PERTURB_VECTOR = 0
 PBN_PERTURB_PER_NODE = 1
+PBN_LAYOUT_AUTO = 0
+PBN_LAYOUT_CHAIN_LANES = 1
+PBN_LAYOUT_NODE_LANES = 2
 PBN_METHOD_TWO_STATE = 0
 PBN_METHOD_SKART = 1
 
@@ -66,7 +69,7 @@ class pbn_sim_args(C.Structure):
                 ("groups_per_cta", C.c_int32), ("warps_per_group", C.c_int32),
                 ("schedule", C.c_int32), ("chunk_steps", C.c_int64), ("n_props", C.c_int32),
                 ("props", C.c_void_p), ("cluster_size", C.c_int32), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_int64)]
+                ("workspace_bytes", C.c_int64), ("layout", C.c_int32), ("chains_per_cluster", C.c_int32)]
 
 
 class pbn_sim_out(C.Structure):

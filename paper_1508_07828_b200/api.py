@@ -224,9 +224,10 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                  init: bool = False, emit_bits: bool = False, bits_offset: int = 0,
                  bits_row_words: int = 0, groups_per_cta: int = 0, warps_per_group: int = 0,
                  schedule: int = 0, chunk_steps: int = 0, stream=None, props=None,
-                 cluster_size: int = 0) -> None:
+                 cluster_size: int = 0, layout: int = 0, chains_per_cluster: int = 0) -> None:
     """props: a list of q >= 1 predicates evaluated on the same trajectories
-    (multi-property reuse); `pred` is then ignored."""
+    (multi-property reuse); `pred` is then ignored.  layout:
+    PBN_LAYOUT_* (0 auto, 1 chains over lanes, 2 nodes over lanes)."""
     cp, _keep = _pred(pred)
     keep_props = None
     n_props, props_ptr = 0, None
@@ -240,7 +241,8 @@ def pbn_simulate(model: Model, out: SimOutputs, *, n_chains: int, steps: int, ch
                        emit_bits=int(bool(emit_bits)), bits_offset=bits_offset,
                        bits_row_words=bits_row_words, groups_per_cta=groups_per_cta,
                        warps_per_group=warps_per_group, schedule=schedule, chunk_steps=chunk_steps,
-                       n_props=n_props, props=props_ptr, cluster_size=cluster_size)
+                       n_props=n_props, props=props_ptr, cluster_size=cluster_size, layout=layout,
+                       chains_per_cluster=chains_per_cluster)
     _check_outputs(model, out, n_chains=n_chains, steps=steps, batch=batch, emit_bits=emit_bits,
                    bits_offset=bits_offset, bits_row_words=bits_row_words, n_props=n_props)
     if out.workspace is not None:

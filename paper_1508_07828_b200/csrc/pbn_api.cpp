@@ -25,6 +25,17 @@ struct ClusterImages {
     uint32_t max_bytes = 0;
 };
 
+// Packed sub-images of one cluster size K for the lanes-over-nodes kernel
+// (pbn_nodepar.cu): rank r owns packed state words [w_lo[r], w_lo[r+1]).
+struct NodeParImages {
+    int K = 0;
+    uint8_t* d_buf = nullptr;
+    uint32_t off[pbn::kMaxCluster] = {}, bytes[pbn::kMaxCluster] = {}, reloc_off[pbn::kMaxCluster] = {};
+    int32_t reloc_count[pbn::kMaxCluster] = {};
+    int32_t w_lo[pbn::kMaxCluster + 1] = {};
+    uint32_t max_bytes = 0;
+};
+
 struct pbn_model_s {
     int device = 0;
     pbn::ImageLayout L;
@@ -33,6 +44,7 @@ struct pbn_model_s {
     uint32_t flags = 0;
     int64_t n_parents = 0;
     std::vector<ClusterImages> clusters;  // K = 2, 4, 8, 16 (K <= quads)
+    std::vector<NodeParImages> nodepar;   // K = 1, 2, 4, 8, 16 (K <= packed words)
 };
 
 namespace {
@@ -210,7 +222,7 @@ inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
 // 48: three buffers, pbn_cluster).  The fast width FT and the slow-node
 // count are model-wide, so every sub-image of a cluster uses one kernel.
 std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L, int32_t node_lo = 0,
-                                 int32_t node_hi = -1, uint32_t qs = 32)
+                                 int32_t node_hi = -1, uint32_t qs = 32, bool packed = false)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
     if (node_hi < 0) node_hi = n;
@@ -262,12 +274,13 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                 uint32_t* w = B.u32(off_desc + ds * (uint32_t)j);
                 const uint32_t wbase = off_desc + ds * (uint32_t)j;
                 auto par = [&](int32_t m) {
-                    return pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u, qs);
+                    const uint32_t node = m < theta ? d->parents[d->par_off[f] + m] : 0u;
+                    return packed ? node : pbn::state_off(node, qs);
                 };
                 if (tm >= 7) {
                     // {a[0..7] (a[7] padding when FT = 7), table words}
                     for (int32_t m = 0; m < 8; ++m) {
-                        reloc.push_back((wbase + 4u * (uint32_t)m) | pbn::kRelocState);
+                        if (!packed) reloc.push_back((wbase + 4u * (uint32_t)m) | pbn::kRelocState);
                         w[m] = par(m < tm ? m : tm);
                     }
                     // stored bit-reversed per word: entry e at bit 31 - (e & 31)
@@ -278,7 +291,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                     if (tm == 6) w[k++] = reverse_bits(T[1]);
                     // padded parent list, MSB first, relocated by the state base
                     for (int32_t m = 0; m < tm; ++m) {
-                        reloc.push_back((wbase + 4u * (uint32_t)k) | pbn::kRelocState);
+                        if (!packed) reloc.push_back((wbase + 4u * (uint32_t)k) | pbn::kRelocState);
                         w[k++] = par(m);
                     }
                 }
@@ -296,7 +309,10 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                 const uint32_t off_t = B.alloc(4u * words, 4);
                 for (int32_t w = 0; w < words; ++w) B.u32(off_t)[w] = d->tables[d->tbl_off[f] + w];
                 const uint32_t off_p = B.alloc(4u * (size_t)std::max(theta, 1), 4);
-                for (int32_t m = 0; m < theta; ++m) B.u32(off_p)[m] = pbn::state_off(d->parents[d->par_off[f] + m], qs);
+                for (int32_t m = 0; m < theta; ++m) {
+                    const uint32_t node = d->parents[d->par_off[f] + m];
+                    B.u32(off_p)[m] = packed ? node : pbn::state_off(node, qs);
+                }
                 uint32_t* gd = B.u32(off_gd + 16u * j);
                 gd[0] = off_t;
                 gd[1] = (uint32_t)theta;
@@ -419,6 +435,39 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
         }
         m->clusters.push_back(ci);
     }
+    // packed sub-images for the lanes-over-nodes kernel: CTA r of a K-cluster
+    // owns packed state words [W r / K, W (r+1) / K)
+    const int32_t nw = (desc->n + 31) / 32;
+    for (int K = 1; K <= pbn::kMaxCluster && K <= nw; K *= 2) {
+        NodeParImages ni;
+        ni.K = K;
+        std::vector<uint8_t> all;
+        for (int r = 0; r <= K; ++r) ni.w_lo[r] = (int32_t)((int64_t)nw * r / K);
+        for (int r = 0; r < K; ++r) {
+            pbn::ImageLayout Lr;
+            const int32_t lo = 32 * ni.w_lo[r], hi = std::min(desc->n, 32 * ni.w_lo[r + 1]);
+            std::vector<uint8_t> sub = build_image(desc, m->Tp, &Lr, lo, hi, 32u, true);
+            const size_t off = (all.size() + 15) & ~(size_t)15;
+            all.resize(off + sub.size(), 0);
+            std::memcpy(all.data() + off, sub.data(), sub.size());
+            ni.off[r] = (uint32_t)off;
+            ni.bytes[r] = Lr.bytes;
+            ni.reloc_off[r] = Lr.reloc_off;
+            ni.reloc_count[r] = Lr.reloc_count;
+            ni.max_bytes = std::max(ni.max_bytes, Lr.bytes);
+        }
+        if (cudaMalloc(&ni.d_buf, all.size()) != cudaSuccess ||
+            cudaMemcpy(ni.d_buf, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            if (ni.d_buf) cudaFree(ni.d_buf);
+            for (auto& c : m->nodepar) cudaFree(c.d_buf);
+            for (auto& c : m->clusters) cudaFree(c.d_buf);
+            cudaFree(m->d_image);
+            delete m;
+            set_err(err, errlen, "node-parallel sub-image upload failed");
+            return PBN_E_CUDA;
+        }
+        m->nodepar.push_back(ni);
+    }
     *out = m;
     return PBN_OK;
 }
@@ -428,6 +477,7 @@ void pbn_free(pbn_model model)
     if (!model) return;
     if (model->d_image) cudaFree(model->d_image);
     for (auto& c : model->clusters) cudaFree(c.d_buf);
+    for (auto& c : model->nodepar) cudaFree(c.d_buf);
     delete model;
 }
 
@@ -535,6 +585,77 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         return PBN_E_CUDA;
     const size_t limit = (size_t)smem_optin - 64;
     const int64_t groups = (a->n_chains + 31) / 32;
+    if (a->layout < PBN_LAYOUT_AUTO || a->layout > PBN_LAYOUT_NODE_LANES) return PBN_E_USAGE;
+    // ---- lanes over nodes (K1n): G chains per cluster of K CTAs ----
+    const int32_t nw = (P.n + 31) / 32;
+    if (a->chains_per_cluster < 0 || a->chains_per_cluster > 32) return PBN_E_USAGE;
+    auto np_fits = [&](const NodeParImages& ni, int G) {
+        return pbn::nodepar_smem_bytes(nw, G, ni.max_bytes) <= limit;
+    };
+    // chains per cluster: enough to put one CTA on every SM (a wave of
+    // clusters), at most 32 and what the shared memory holds
+    auto np_G = [&](const NodeParImages& ni) {
+        int G = a->chains_per_cluster;
+        if (G == 0) G = (int)std::min<int64_t>(32, std::max<int64_t>(1, (a->n_chains * ni.K + sms - 1) / sms));
+        while (G > 1 && !np_fits(ni, G)) --G;
+        return G;
+    };
+    // auto cluster size: the smallest K whose sub-image fits, raised while
+    // the clusters still fit one wave on the SMs and every CTA keeps >= 4
+    // packed words (128 nodes) -- measured (profiles/nodelanes_r2.jsonl):
+    // 1 chain of C3-C5 is fastest at K = 8-16, 64 chains at K = 2 (C5: the
+    // fitting 4), 256 chains at the smallest fitting K with G = 2
+    auto np_auto = [&]() -> const NodeParImages* {
+        const NodeParImages* use = nullptr;
+        for (const auto& ni : m->nodepar) {
+            if (!np_fits(ni, 1)) continue;
+            if (!use || (a->n_chains * ni.K <= sms && nw >= 4 * ni.K)) use = &ni;
+        }
+        return use;
+    };
+    // auto layout (cluster_size 0): lanes over nodes for few chains --
+    // measured faster than the chain-lanes kernels up to 256 chains (up to 64
+    // for n > 2048: C5 at 256 chains favours the cluster kernel K1c)
+    const bool node_lanes = a->layout == PBN_LAYOUT_NODE_LANES ||
+                            (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 && a->n_chains <= 256 &&
+                             (a->n_chains <= 64 || P.n <= 2048));
+    const NodeParImages* np_use = nullptr;
+    if (node_lanes) {
+        if (a->cluster_size >= 1) {
+            for (const auto& ni : m->nodepar)
+                if (ni.K == a->cluster_size) np_use = &ni;
+            if (!np_use || !np_fits(*np_use, 1)) return PBN_E_USAGE;
+        } else {
+            np_use = np_auto();
+            if (!np_use && a->layout == PBN_LAYOUT_NODE_LANES) return PBN_E_USAGE;
+        }
+    }
+    if (np_use) {
+        pbn::NodeParParams C;
+        std::memset(&C, 0, sizeof(C));
+        C.T = P;
+        C.T.image = np_use->d_buf;
+        C.K = np_use->K;
+        C.G = np_G(*np_use);
+        if (a->chains_per_cluster > 0 && C.G != a->chains_per_cluster) return PBN_E_USAGE;
+        C.n_words = nw;
+        int ow = 0;
+        for (int r = 0; r < np_use->K; ++r) {
+            C.img_off[r] = np_use->off[r];
+            C.img_bytes[r] = np_use->bytes[r];
+            C.reloc_off[r] = np_use->reloc_off[r];
+            C.reloc_count[r] = np_use->reloc_count[r];
+            ow = std::max(ow, np_use->w_lo[r + 1] - np_use->w_lo[r]);
+        }
+        for (int r = 0; r <= np_use->K; ++r) C.w_lo[r] = np_use->w_lo[r];
+        // one warp per (chain, own word) -- up to 32 warps, which then loop
+        int threads = std::min(1024, 32 * C.G * ow);
+        if (a->warps_per_group > 0) threads = std::min(1024, 32 * a->warps_per_group);
+        threads = std::max(threads, 32 * P.n_props);
+        const size_t smem = pbn::nodepar_smem_bytes(nw, C.G, np_use->max_bytes);
+        const int rc = pbn::launch_traj_nodepar(C, threads, smem, stream);
+        return rc == 0 ? PBN_OK : PBN_E_CUDA;
+    }
     auto fits = [&](const ClusterImages& ci) { return pbn::cluster_smem_bytes(P, ci.max_bytes) <= limit; };
     const ClusterImages* use = nullptr;
     if (a->cluster_size >= 2) {

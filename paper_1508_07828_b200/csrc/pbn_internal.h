@@ -33,6 +33,10 @@
 //   generic descriptor (uint4)          {toff, theta, poff, 0}
 //       toff   offset of the ceil(2^theta/32) table words; poff: u32 list of
 //              state_off(parent), parents[0] first (MSB, reading Q5)
+//   PACKED form (pbn_nodepar.cu, lanes over nodes): identical, except that a
+//       parent entry a[m] (and a generic descriptor's poff list) holds the
+//       parent's NODE ID -- the state is bit-packed, node i = bit i & 31 of
+//       word i >> 5 -- and is not relocated
 //   relocation list (u32, stored after the image in device memory, not staged)
 //       byte offsets of every image-offset-valued word above (nrec.w, thr,
 //       gdesc, toff, poff) and, flagged with kRelocState, of every fast
@@ -154,6 +158,24 @@ struct ClusterParams {
 size_t cluster_smem_bytes(const TrajParams& P, uint32_t max_sub_image);
 int launch_traj_cluster(const ClusterParams& C, int warps, size_t smem_bytes, void* stream);
 int max_active_clusters(const ClusterParams& C, int warps, size_t smem_bytes, int* out);
+
+// Lanes-over-nodes launch (pbn_nodepar.cu): G chains per cluster of K CTAs,
+// CTA rank r owns the packed state words [w_lo[r], w_lo[r+1]) (nodes
+// 32 w_lo[r] ..) and stages sub-image r, built in the packed form.
+struct NodeParParams {
+    TrajParams T;               // T.image = base of the K concatenated packed sub-images
+    int32_t K;
+    int32_t G;                  // chains per cluster (1..32; cluster c runs chains c G ..)
+    int32_t n_words;            // ceil(n/32)
+    uint32_t img_off[kMaxCluster];
+    uint32_t img_bytes[kMaxCluster];
+    uint32_t reloc_off[kMaxCluster];
+    int32_t reloc_count[kMaxCluster];
+    int32_t w_lo[kMaxCluster + 1];
+};
+size_t nodepar_smem_bytes(int n_words, int G, uint32_t max_sub_image);
+int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, void* stream);
+int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem_bytes, int* out);
 
 struct LaunchPlan {
     int warps_per_group;

@@ -1,0 +1,4 @@
+TAG=${1:-r2f}
+mkdir -p gpurun_out
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:nodepar -s 1 -c 1 -o gpurun_out/prof_np_C5x64_$TAG python scripts/run_nodelanes.py C5 64 4 1000 2 > gpurun_out/ncu_np_C5x64_$TAG.log 2>&1; echo "ncu rc=$?"
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:nodepar -s 1 -c 1 -o gpurun_out/prof_np_C5x1_$TAG python scripts/run_nodelanes.py C5 1 16 1000 1 > gpurun_out/ncu_np_C5x1_$TAG.log 2>&1; echo "ncu rc=$?"

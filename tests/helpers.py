@@ -38,7 +38,8 @@ def sample_chain_ids(n_chains: int, k: int = 8, seed: int = 0) -> list[int]:
 
 def gpu_run(pm, model, pred, *, n_chains, steps, burn_in=0, step0=0, chain_base=0, seed=1, batch=0,
             emit_bits=True, init=True, state=None, groups=0, warps=0, bits_offset=0,
-            bits_row_words=0, bits_init=None, schedule=0, chunk_steps=0, props=None, cluster_size=0):
+            bits_row_words=0, bits_init=None, schedule=0, chunk_steps=0, props=None, cluster_size=0, layout=0,
+            chains_per_cluster=0):
     """Run pbn_simulate; returns a dict of host numpy arrays (with `props`,
     every field but state has a leading property dimension)."""
     import torch
@@ -53,7 +54,8 @@ def gpu_run(pm, model, pred, *, n_chains, steps, burn_in=0, step0=0, chain_base=
                      burn_in=burn_in, batch=batch, seed=seed, pred=pred, init=init,
                      emit_bits=emit_bits, bits_offset=bits_offset, bits_row_words=bits_row_words,
                      groups_per_cta=groups, warps_per_group=warps, schedule=schedule,
-                     chunk_steps=chunk_steps, props=props, cluster_size=cluster_size)
+                     chunk_steps=chunk_steps, props=props, cluster_size=cluster_size, layout=layout,
+                     chains_per_cluster=chains_per_cluster)
     torch.cuda.synchronize()
 
     def h(t):

@@ -387,3 +387,81 @@ def test_extreme_perturbation_probabilities(pbn, p):
     pred = Predicate(np.array([0, 1], np.uint16), np.array([1, 1], np.uint8))
     for per_node in (False, True):
         full_compare(pbn, model, pred, n_chains=40, steps=300, burn_in=10, seed=6, batch=25, per_node=per_node)
+
+
+# --------------------------------------------------------------------------
+# K1n: lanes over nodes, one chain per cluster of K CTAs (pbn_nodepar.cu)
+# --------------------------------------------------------------------------
+NODE_LANES = 2
+
+
+@pytest.mark.parametrize("K,G", [(1, 1), (2, 1), (4, 1), (1, 2), (2, 3), (4, 32), (1, 0)])
+@pytest.mark.parametrize("per_node", [False, True])
+def test_node_lanes_kernel_equals_chain_lanes_and_oracle(pbn, K, G, per_node):
+    """The lanes-over-nodes kernel gives exactly the chain-lanes kernel's
+    outputs (A12: launch-shape independence across layouts) for every
+    cluster size K and chains per cluster G (37 chains: a ragged last
+    cluster), with several properties, and matches the oracle."""
+    model = config_model("C2")
+    props = random_props(model, 3, np.random.default_rng(K + 10 * per_node + 100 * G))
+    pm = load(pbn, model, per_node)
+    kw = dict(n_chains=37, steps=444, burn_in=55, seed=12, batch=40, props=props)
+    a = gpu_run(pm, model, None, cluster_size=1, layout=1, **kw)
+    b = gpu_run(pm, model, None, cluster_size=K, layout=NODE_LANES, chains_per_cluster=G, **kw)
+    for k in ["state"] + FIELDS:
+        assert np.array_equal(a[k], b[k]), (K, G, k)
+    ids = [0, 1, 2, 35, 36]
+    st, I, ws = oracle_run(model, props[0], ids, steps=444, burn_in=55, seed=12, batch=40, per_node=per_node)
+    packed = pack_states(st)
+    first = {k: (b[k][0] if k != "state" else b[k]) for k in ["state"] + FIELDS}
+    for j, c in enumerate(ids):
+        compare_chain(first, c, packed[j], ws[j], 444, 40)
+
+
+@pytest.mark.parametrize("per_node", [False, True])
+@pytest.mark.parametrize("name,model,pred", list(edge_models()), ids=[e[0] for e in edge_models()])
+def test_node_lanes_edge_models(pbn, name, model, pred, per_node):
+    """Every fast width FT = 3..8, the generic (slow) path, ragged quads,
+    n = 1, constant functions, heavy perturbation -- lanes over nodes vs the
+    oracle on every chain."""
+    pm = load(pbn, model, per_node)
+    g = gpu_run(pm, model, pred, n_chains=6, steps=555, burn_in=77, seed=19, batch=50, layout=NODE_LANES)
+    st, I, ws = oracle_run(model, pred, np.arange(6), steps=555, burn_in=77, seed=19, batch=50, per_node=per_node)
+    packed = pack_states(st)
+    for c in range(6):
+        compare_chain(g, c, packed[c], ws[c], 555, 50)
+    assert np.array_equal(g["totals"], ostats.totals(ws))
+
+
+def test_node_lanes_continuation_and_chain_base(pbn):
+    """Chains continue exactly across calls and layouts (init=False, step0 > 0,
+    chain_base > 0, bits appended at an offset)."""
+    model, pred = config_model("C3"), config_predicate("C3")
+    pm = load(pbn, model)
+    s1 = gpu_run(pm, model, pred, n_chains=3, chain_base=40, steps=300, seed=8, layout=NODE_LANES,
+                 bits_row_words=30)
+    s2 = gpu_run(pm, model, pred, n_chains=3, chain_base=40, steps=500, step0=300, seed=8, init=False,
+                 state=s1["state"], batch=25, layout=NODE_LANES, cluster_size=4, bits_offset=300, bits_row_words=30,
+                 bits_init=s1["bits"])
+    full = gpu_run(pm, model, pred, n_chains=3, chain_base=40, steps=800, seed=8, layout=1, cluster_size=1)
+    assert np.array_equal(s2["state"], full["state"])
+    assert np.array_equal(s2["bits"][:, :25], full["bits"][:, :25])
+    st, I, ws = oracle_run(model, pred, [40, 41, 42], steps=800, seed=8)
+    assert np.array_equal(s2["state"], pack_states(st))
+
+
+@pytest.mark.parametrize("K", [8, 16])
+def test_node_lanes_C5(pbn, K):
+    """C5 (n = 5000, image 871 KB: sub-images of 1/8 or 1/16 per CTA) with
+    lanes over nodes: 1 and 3 chains at the sweep's 10^4 steps vs the oracle."""
+    c = CONFIGS["C5"]
+    model, pred = config_model("C5"), config_predicate("C5")
+    pm = load(pbn, model)
+    for chains, G in ((1, 1), (3, 1), (5, 2)):
+        g = gpu_run(pm, model, pred, n_chains=chains, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed,
+                    batch=c.batch, layout=NODE_LANES, cluster_size=K, chains_per_cluster=G)
+        st, I, ws = oracle_run(model, pred, np.arange(chains), steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed,
+                               batch=c.batch, threads=os.cpu_count() or 8)
+        packed = pack_states(st)
+        for j in range(chains):
+            compare_chain(g, j, packed[j], ws[j], c.steps, c.batch)
