@@ -40,24 +40,37 @@ SM_COUNT_B200 = 148
 def demand_per_node_update(model) -> dict:
     """Algorithmic demand per node-update, SURVEY §8(d) (declared from the
     method and the one-word-per-node-update stream of reading Q3, not from the
-    achieved SASS):
+    achieved SASS), averaged over the nodes:
       RNG     1/4 Philox4x32-10 = 5 IMAD.WIDE (FMA pipe) + 5 LOP3 (ALU)
-      decide  1 compare against T_p + (ell-1) compares/selects ~ ell + 1
+      decide  1 compare against T_p + (ell-1) compares/selects ~ ell + 1;
+              nodes of the generic (dense, NEXT-3) path: a binary search,
+              3 ops per step, ceil(log2 ell) steps
       gather  2 per parent of the selected function (extract + insert)
       lookup  2 (+1 word select when the selected function has theta >= 6)
       commit  1
     smem: (theta_sel + 1)/32 wavefronts (one state word per selected parent
     and one metadata read, each serving the 32 chains of a bit-sliced word).
+    Image bytes (nodes of the generic path, image read through L1/L2): per
+    lane the binary search's thresholds (4 B per step), the selected
+    function's descriptor (16 B), its parent offsets (4 B each) and one
+    table word (4 B); the node record (16 B) is shared by the 32 lanes.
     theta_sel, [theta >= 6] are weighted by the selection probabilities."""
     ell = np.diff(model.fn_off).astype(np.float64)
     theta = np.diff(model.par_off).astype(np.float64)
     node_of_fn = np.repeat(np.arange(model.n), np.diff(model.fn_off))
-    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n).mean()
-    sel_big = np.bincount(node_of_fn, weights=model.sel_prob * (theta >= 6), minlength=model.n).mean()
-    alu = 5.0 + (ell.mean() + 1.0) + 2.0 * sel_theta + 2.0 + sel_big + 1.0
+    sel_theta = np.bincount(node_of_fn, weights=model.sel_prob * theta, minlength=model.n)
+    sel_big = np.bincount(node_of_fn, weights=model.sel_prob * (theta >= 6), minlength=model.n)
+    thmax = np.zeros(model.n)
+    np.maximum.at(thmax, node_of_fn, theta)
+    slow = (ell > 4) | (thmax > 8)                       # the generic (dense) path
+    steps = np.ceil(np.log2(np.maximum(ell, 1.0)))
+    decide = np.where(slow, 1.0 + 3.0 * steps, ell + 1.0)
+    alu = (5.0 + decide + 2.0 * sel_theta + 2.0 + sel_big + 1.0).mean()
     fma = 5.0
-    return {"alu": float(alu), "fma": fma, "issue": float(alu + fma), "lds_wavefronts": float((sel_theta + 1.0) / 32.0),
-            "theta_sel": float(sel_theta), "ell": float(ell.mean())}
+    img_bytes = np.where(slow, 16.0 / 32 + 4.0 * steps + 16.0 + 4.0 * sel_theta + 4.0, 0.0).mean()
+    return {"alu": float(alu), "fma": fma, "issue": float(alu + fma),
+            "lds_wavefronts": float((sel_theta.mean() + 1.0) / 32.0), "image_bytes": float(img_bytes),
+            "theta_sel": float(sel_theta.mean()), "ell": float(ell.mean()), "dense_nodes": float(slow.mean())}
 
 
 def load_peaks() -> dict:
@@ -93,6 +106,9 @@ def roofline(model, node_updates: float, kernel_s: float, sm_mhz: float) -> dict
         "issue": (pk["issue_warp_instr_per_clk"] * 32 * hz, d["issue"], "Tinstr/s"),
         "smem": (pk["lds_wavefronts_per_clk"] * hz, d["lds_wavefronts"], "Twavefronts/s"),
     }
+    if d["image_bytes"] > 0 and pk.get("l2_read_gbs"):
+        # generic-path nodes read their image through L1/L2 (the dense class)
+        res["l2"] = (pk["l2_read_gbs"] * 1e9, d["image_bytes"], "TB/s")
     rate = node_updates / kernel_s
     per = {k: {"peak": P / 1e12, "demand_per_node_update": D, "roofline_node_updates_per_s": P / D,
                "frac": rate * D / P, "unit": U} for k, (P, D, U) in res.items()}

@@ -325,7 +325,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
             sr[0] = off_thr;
             sr[1] = (uint32_t)ell;
             sr[2] = off_gd;
-            sr[3] = 0;
+            sr[3] = (uint32_t)thmax[i];  // warp-uniform gather trip count
             reloc.push_back(off_slow);
             reloc.push_back(off_slow + 8u);
             w3 = off_slow | pbn::kSlowNode;

@@ -27,7 +27,7 @@
 //              kernel reads an entry as the sign bit of (word << (e & 31))
 //       a[m]   state_off(parent m), MSB first (parents[0] first, reading Q5);
 //              the pad entries read node 0
-//   slow record (uint4, per slow node)  {thr, ell, gdesc, 0}
+//   slow record (uint4, per slow node)  {thr, ell, gdesc, theta_max}
 //       thr    offset of ell-1 u32 thresholds E_1..E_{ell-1}
 //       gdesc  offset of ell generic descriptors
 //   generic descriptor (uint4)          {toff, theta, poff, 0}

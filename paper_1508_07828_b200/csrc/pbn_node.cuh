@@ -191,21 +191,31 @@ struct Img {
     }
 };
 
-// Generic path for nodes outside the fast shape (ell > 4 or theta_max > 6).
-// `old` = address of buffer-0 word of node 0 plus the old buffer's offset.
+// Generic path for nodes outside the fast shape (ell > 4 or theta_max > 8:
+// the dense class of P:605-609, NEXT-3).  `old` = address of buffer-0 word
+// of node 0 plus the old buffer's offset.  Every loop has a warp-uniform
+// trip count (the lanes' chains select different functions):
+//   A5  j = #{k : u > E_k} by a binary search over the node's ell-1
+//       ascending thresholds, ceil(log2 ell) steps
+//   A6  theta_max(node) gather steps, predicated on m < theta of the
+//       selected function
 template <bool SMEM>
 __device__ __noinline__ uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w, uint32_t u, uint32_t old,
                                                uint32_t rot)
 {
-    const uint4 sr = img.ld128(w & ~15u);  // {thr, ell, gdesc, 0}
+    const uint4 sr = img.ld128(w & ~15u);  // {thr, ell, gdesc, theta_max}
+    const uint32_t m1 = sr.y - 1u;         // thresholds E_1..E_{ell-1}
     uint32_t j = 0;
-    for (uint32_t k = 0; k + 1 < sr.y; ++k) j += (uint32_t)(u > img.ld32(sr.x + 4u * k));
+    for (uint32_t step = m1 ? 1u << (31 - __clz(m1)) : 0u; step; step >>= 1)
+        if (j + step <= m1 && u > img.ld32(sr.x + 4u * (j + step - 1u))) j += step;
     const uint4 gd = img.ld128(sr.z + 16u * j);  // {toff, theta, poff, 0}
     uint32_t idx = 0;
-    for (uint32_t m = 0; m < gd.y; ++m) {
-        const uint32_t off = img.ld32(gd.z + 4u * m);
-        const uint32_t wv = lds32(old + off);
-        idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+    for (uint32_t m = 0; m < sr.w; ++m) {
+        if (m < gd.y) {
+            const uint32_t off = img.ld32(gd.z + 4u * m);
+            const uint32_t wv = lds32(old + off);
+            idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+        }
     }
     const uint32_t tw = img.ld32(gd.x + 4u * (idx >> 5));
     return (tw >> (idx & 31u)) & 1u;

@@ -145,13 +145,16 @@ __device__ __forceinline__ uint32_t fast_bit_packed(uint32_t dp, uint32_t S)
     return (uint32_t)((int32_t)(tw << idx) < 0);
 }
 
-// generic node (ell > 4 or theta_max > 8): slow record {thr, ell, gdesc, 0},
-// generic descriptors {toff, theta, poff, 0}, poff = parent node ids
+// generic node (ell > 4 or theta_max > 8): slow record {thr, ell, gdesc,
+// theta_max}, generic descriptors {toff, theta, poff, 0}, poff = parent node
+// ids; binary-search selection (ascending thresholds), as slow_node_bit
 __device__ __noinline__ uint32_t slow_bit_packed(uint32_t w, uint32_t u, uint32_t S)
 {
     const uint4 sr = lds128_ro(w & ~15u);
+    const uint32_t m1 = sr.y - 1u;
     uint32_t j = 0;
-    for (uint32_t k = 0; k + 1 < sr.y; ++k) j += (uint32_t)(u > lds32_ro(sr.x + 4u * k));
+    for (uint32_t step = m1 ? 1u << (31 - __clz(m1)) : 0u; step; step >>= 1)
+        if (j + step <= m1 && u > lds32_ro(sr.x + 4u * (j + step - 1u))) j += step;
     const uint4 gd = lds128_ro(sr.z + 16u * j);
     uint32_t idx = 0;
     for (uint32_t m = 0; m < gd.y; ++m) idx = 2u * idx + pbit(S, lds32_ro(gd.z + 4u * m));

@@ -465,3 +465,53 @@ def test_node_lanes_C5(pbn, K):
         packed = pack_states(st)
         for j in range(chains):
             compare_chain(g, j, packed[j], ws[j], c.steps, c.batch)
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: the dense class (density 150-300): the generic path
+# with binary-search selection and warp-uniform gathers
+# --------------------------------------------------------------------------
+def test_dense_class_C6_sampled_chains(pbn):
+    """C6 (n = 1000, ell ~ U{8..24}, theta ~ U{8..12}, density ~160; image
+    ~5 MB read through L1/L2) in bench.py's launch configuration, 32 sampled
+    chains against the oracle at the full step count, invariants on all."""
+    c = CONFIGS["C6"]
+    model, pred = config_model("C6"), config_predicate("C6")
+    pm = load(pbn, model)
+    g = gpu_run(pm, model, pred, n_chains=c.chains, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch)
+    ids = sample_chain_ids(c.chains, k=32, seed=c.sim_seed)
+    st, I, ws = oracle_run(model, pred, ids, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch,
+                           threads=os.cpu_count() or 8)
+    packed = pack_states(st)
+    for k, cid in enumerate(ids):
+        compare_chain(g, cid, packed[k], ws[k], c.steps, c.batch)
+    c1 = g["c1"].astype(np.int64)
+    assert np.array_equal(g["batch_sums"].astype(np.int64).sum(axis=1), c1)
+    assert np.array_equal(np.unpackbits(g["bits"].view(np.uint8), axis=1).sum(axis=1), c1)
+
+
+@pytest.mark.parametrize("per_node", [False, True])
+def test_dense_small_model_every_kernel(pbn, per_node, monkeypatch):
+    """A small dense model (ell up to 20, theta 8..11) through K1 with the
+    image in shared memory, K1 reading it through L1/L2, the cluster kernel
+    and lanes over nodes -- all against the oracle on every chain."""
+    model = random_pbn(70, 5, 20, 8, 11, 0.003, seed=31)
+    pred = Predicate(np.array([0, 69], np.uint16), np.array([1, 0], np.uint8))
+    pm = load(pbn, model, per_node)
+    kw = dict(n_chains=40, steps=500, burn_in=40, seed=5, batch=25)
+    st, I, ws = oracle_run(model, pred, np.arange(40), steps=500, burn_in=40, seed=5, batch=25, per_node=per_node)
+    packed = pack_states(st)
+    runs = {"K1 smem": dict(cluster_size=1), "K1c K=2": dict(cluster_size=2), "K1n": dict(layout=NODE_LANES)}
+    for name, extra in runs.items():
+        try:
+            g = gpu_run(pm, model, pred, **kw, **extra)
+        except Exception as e:  # a layout whose image does not fit shared memory
+            assert "USAGE" in str(e), (name, e)
+            continue
+        for c in range(40):
+            compare_chain(g, c, packed[c], ws[c], 500, 25)
+    monkeypatch.setenv("PBN_FORCE_GLOBAL_IMAGE", "1")
+    g = gpu_run(pm, model, pred, cluster_size=1, **kw)
+    monkeypatch.delenv("PBN_FORCE_GLOBAL_IMAGE")
+    for c in range(40):
+        compare_chain(g, c, packed[c], ws[c], 500, 25)

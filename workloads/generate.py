@@ -1,4 +1,4 @@
-"""Seeded PBN generators and the BASELINE.json configs C1-C5.
+"""Seeded PBN generators, the BASELINE.json configs C1-C5 and C6 (dense class).
 
 Layout of a model (CSR, the same arrays `pbn_load` takes, include/pbnsim.h):
   n         number of nodes (V = (v_1..v_n))
@@ -103,16 +103,24 @@ CONFIGS: dict[str, RunConfig] = {
                     chains=16384, burn_in=0, steps=10_000, batch=100,
                     pred_nodes=(0, 1, 2, 3, 4), pred_values=(1, 0, 1, 0, 1),
                     extra={"chain_sweep": (1, 64, 1024, 16384, 65536)}),
+    # NEXT-3: the paper's DENSE class, density D = 150-300
+    # (P:605-609); ell ~ U{8..24}, theta ~ U{8..12}: D ~ 16 x 10 = 160.
+    # Not a BASELINE.json config (BASELINE's C1-C5 are all sparse).
+    "C6": RunConfig("C6", 1000, (8, 24), (8, 12), 1e-4, "half", 6, 6,
+                    chains=16384, burn_in=5_000, steps=5_000, batch=100,
+                    pred_nodes=(0, 1, 2, 3, 4), pred_values=(1, 0, 1, 0, 1),
+                    extra={"density_class": "dense"}),
 }
 
 
 def _pack_table(bits: np.ndarray) -> np.ndarray:
-    """Pack 0/1 entries (index order) into uint32 words, LSB first."""
-    nbits = len(bits)
-    words = np.zeros((nbits + 31) // 32, dtype=np.uint32)
-    for idx in np.nonzero(bits)[0]:
-        words[idx >> 5] |= np.uint32(1) << np.uint32(idx & 31)
-    return words
+    """Pack 0/1 entries (index order) into uint32 words, LSB first: entry
+    idx is bit (idx & 31) of word idx >> 5."""
+    bits = np.asarray(bits, dtype=np.uint8)
+    nw = (len(bits) + 31) // 32
+    padded = np.zeros(nw * 32, dtype=np.uint8)
+    padded[:len(bits)] = bits
+    return np.packbits(padded, bitorder="little").view("<u4").astype(np.uint32)
 
 
 def model_from_lists(n: int, p: float, nodes: list[list[tuple[list[int], list[int], float]]],
