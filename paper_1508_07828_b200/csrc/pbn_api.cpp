@@ -299,8 +299,11 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
             w3 = off_desc;
         } else {
             const uint32_t off_slow = B.alloc(16);
-            const uint32_t off_thr = B.alloc(4u * std::max<size_t>(E.size(), 1), 4);
-            for (size_t k = 0; k < E.size(); ++k) B.u32(off_thr)[k] = E[k];
+            // thresholds padded with 0xFFFFFFFF to whole 16-byte vectors (the
+            // generic path scans them four at a time; u > 0xFFFFFFFF never holds)
+            const size_t nthr = (std::max<size_t>(E.size(), 1) + 3) & ~(size_t)3;
+            const uint32_t off_thr = B.alloc(4u * nthr, 16);
+            for (size_t k = 0; k < nthr; ++k) B.u32(off_thr)[k] = k < E.size() ? E[k] : 0xFFFFFFFFu;
             const uint32_t off_gd = B.alloc(16u * ell);
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;

@@ -154,7 +154,7 @@ __device__ __noinline__ uint32_t slow_bit_packed(uint32_t w, uint32_t u, uint32_
     const uint32_t m1 = sr.y - 1u;
     uint32_t j = 0;
     for (uint32_t step = m1 ? 1u << (31 - __clz(m1)) : 0u; step; step >>= 1)
-        if (j + step <= m1 && u > lds32_ro(sr.x + 4u * (j + step - 1u))) j += step;
+        if (j + step <= m1 && u > lds32_ro(sr.x + 4u * (j + step - 1u))) j += step;  // lane-divergent anyway
     const uint4 gd = lds128_ro(sr.z + 16u * j);
     uint32_t idx = 0;
     for (uint32_t m = 0; m < gd.y; ++m) idx = 2u * idx + pbit(S, lds32_ro(gd.z + 4u * m));
