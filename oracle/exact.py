@@ -143,3 +143,97 @@ def property_probability(pi: np.ndarray, n: int, pred) -> float:
         if all(((s >> int(node)) & 1) == int(v) for node, v in zip(pred.nodes, pred.values)):
             tot += pi[s]
     return tot
+
+
+# --------------------------------------------------------------------------
+# Geometric-skip perturbation stream (NEXT-2, reading Q18), VECTOR
+# semantics: gamma(t) is drawn as the positions of its ones by successive
+# geometric skips G(v) = #{g < n : Cg[g] <= v}, Cg[g] = floor((1 - q^(g+1))
+# 2^32), q = 1 - p (q^(g+1) by repeated fp64 multiplication); with gamma = 0
+# the nodes select with the unperturbed thresholds Q_j (T_p = 0).
+# --------------------------------------------------------------------------
+def geometric_cdf_table(model) -> list[int]:
+    q, r, out = 1.0 - float(model.p), 1.0, []
+    for _g in range(model.n):
+        r = r * q
+        out.append(int(np.floor(np.ldexp(1.0 - r, 32))))
+    return out
+
+
+def _skip_probs(model):
+    """P(G = g) for g < n and P(G >= L) for L = 0..n, as exact fractions of 2^32."""
+    C = geometric_cdf_table(model)
+    two32 = 1 << 32
+    eq = [(C[g] - (C[g - 1] if g else 0)) / two32 for g in range(model.n)]
+    ge = [1.0] + [(two32 - C[L - 1]) / two32 for L in range(1, model.n + 1)]
+    return eq, ge
+
+
+def geometric_gamma_distribution(model) -> np.ndarray:
+    """P(gamma = v) for every v in {0,1}^n (bit i = node i), closed form:
+    the product of the skip probabilities of v's gaps and of the final
+    skip past node n-1."""
+    n = model.n
+    eq, ge = _skip_probs(model)
+    P = np.zeros(1 << n)
+    for v in range(1 << n):
+        ones = [i for i in range(n) if (v >> i) & 1]
+        pr, prev = 1.0, -1
+        for k in ones:
+            pr *= eq[k - prev - 1]
+            prev = k
+        pr *= ge[n - prev - 1]
+        P[v] = pr
+    return P
+
+
+def geometric_gamma_by_enumeration(model) -> np.ndarray:
+    """The same distribution by enumerating every outcome of the skip
+    process (draw after draw) -- an independent construction."""
+    n = model.n
+    eq, ge = _skip_probs(model)
+    P = np.zeros(1 << n)
+
+    def walk(k, v, pr):       # next candidate position k, flips so far v
+        P_stop = ge[n - k]     # G >= n - k: no further flip
+        P[v] += pr * P_stop
+        for g in range(n - k):
+            walk(k + g + 1, v | (1 << (k + g)), pr * eq[g])
+
+    walk(0, 0, 1.0)
+    return P
+
+
+def unperturbed_selection_probs(model) -> np.ndarray:
+    """c_q[f] realised by the node word with T_p = 0: (Q_j - Q_{j-1}) / 2^32."""
+    two32 = 1 << 32
+    c_q = np.zeros(model.nf)
+    for i in range(model.n):
+        f0, f1 = int(model.fn_off[i]), int(model.fn_off[i + 1])
+        prevQ, C = 0, 0.0
+        for f in range(f0, f1):
+            C = C + float(model.sel_prob[f])
+            Q = two32 if f == f1 - 1 else min(int(np.floor(np.ldexp(C, 32))), two32)
+            c_q[f] = (Q - prevQ) / two32
+            prevQ = Q
+    return c_q
+
+
+def matrix_geometric(model, gamma_probs=None) -> np.ndarray:
+    """T(s, s') = P_gamma(s XOR s') [s' != s] + P_gamma(0) prod_i P(f_i(s) = s'_i)
+    (VECTOR semantics, with gamma from the skip stream)."""
+    n = model.n
+    S = 1 << n
+    Pg = geometric_gamma_distribution(model) if gamma_probs is None else gamma_probs
+    c = unperturbed_selection_probs(model)
+    states = np.arange(S)
+    bits = ((states[:, None] >> np.arange(n)[None, :]) & 1).astype(np.float64)
+    T = np.zeros((S, S))
+    for s in range(S):
+        q = np.array([sum(c[f] * _fn_value(model, f, s) for f in range(model.fn_off[i], model.fn_off[i + 1]))
+                      for i in range(n)])
+        fn = np.prod(bits * q[None, :] + (1 - bits) * (1 - q[None, :]), axis=1)
+        pert = Pg[states ^ s].copy()
+        pert[s] = 0.0
+        T[s] = pert + Pg[0] * fn
+    return T

@@ -22,7 +22,9 @@
  *     thresholds (reading Q3);
  *   - truth-table lookup with parents[0] as the most significant index
  *     bit (reading Q5);
- *   - the property indicator I_t = AND_k [s_t[node_k] = v_k].
+ *   - the property indicator I_t = AND_k [s_t[node_k] = v_k];
+ *   - optionally (NEXT-2, reading Q18) gamma(t) drawn by geometric skips
+ *     from a separate word stream, VECTOR semantics.
  *
  * Statistics (counts, transitions, batches, R-hat, two-state, Skart) are
  * computed in Python by definition from the stored I sequence
@@ -122,6 +124,66 @@ void oracle_selection_thresholds(int32_t n, const int32_t* fn_off, const double*
 }
 
 /* ------------------------------------------------------------------ */
+/* Geometric-skip perturbation stream (SPEC S:177's optional mode,      */
+/* SURVEY NEXT-2; reading Q18), VECTOR semantics.             */
+/* The perturbation vector gamma(t) in {0,1}^n with i.i.d. Bernoulli(p) */
+/* components is drawn as the positions of its ones:        */
+/*   k_1 = G(v_0),  k_{j+1} = k_j + 1 + G(v_j),  stop at the first k>=n */
+/* where G(v) = #{g in [0,n) : Cg[g] <= v} is a geometric skip drawn    */
+/* from one 32-bit word v by inverting the cumulative table             */
+/*   Cg[g] = floor((1 - q^(g+1)) * 2^32),  q = 1 - p,                   */
+/* with q^(g+1) formed by repeated fp64 multiplication (q, q*q, ...).   */
+/* The skip words are a separate Philox counter space:                  */
+/*   v(chain, t, m) = philox((2^31 + m/4, chain, t lo, t hi), key)[m%4] */
+/* When gamma(t) = 0 every node selects function j = min{j : u < Q_j}   */
+/* with its node word u(chain, t, i) (reading Q3 with T_p = 0).         */
+/* ------------------------------------------------------------------ */
+void oracle_geometric_table(int32_t n, double p, uint32_t* Cg)
+{
+    double q = 1.0 - p, r = 1.0;
+    for (int32_t g = 0; g < n; ++g) {
+        r = r * q; /* q^(g+1) */
+        Cg[g] = (uint32_t)floor(ldexp(1.0 - r, 32));
+    }
+}
+
+uint32_t oracle_skip_word(uint64_t seed, uint32_t chain, uint64_t t, uint32_t m)
+{
+    uint32_t ctr[4] = {0x80000000u + m / 4u, chain, (uint32_t)(t & 0xFFFFFFFFu), (uint32_t)(t >> 32)};
+    uint32_t key[2] = {(uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    oracle_philox4x32_10(ctr, key, out);
+    return out[m % 4u];
+}
+
+/* G(v): the number of table entries <= v, by a plain linear count */
+int32_t oracle_skip(const uint32_t* Cg, int32_t n, uint32_t v)
+{
+    int32_t G = 0;
+    for (int32_t g = 0; g < n; ++g)
+        if (Cg[g] <= v)
+            G++;
+    return G;
+}
+
+/* gamma(t) of one chain-step into gam[0..n-1]; returns the number of ones */
+static int32_t geometric_gamma(const uint32_t* Cg, int32_t n, uint64_t seed, uint32_t chain, uint64_t t,
+                               uint8_t* gam)
+{
+    memset(gam, 0, (size_t)n);
+    int32_t ones = 0;
+    int64_t k = -1;
+    for (uint32_t m = 0;; ++m) {
+        k = k + 1 + oracle_skip(Cg, n, oracle_skip_word(seed, chain, t, m));
+        if (k >= n)
+            break;
+        gam[k] = 1;
+        ones++;
+    }
+    return ones;
+}
+
+/* ------------------------------------------------------------------ */
 /* One synchronous step with given words u[0..n-1].        */
 /* ------------------------------------------------------------------ */
 typedef struct {
@@ -210,16 +272,23 @@ int oracle_simulate(int32_t n, const int32_t* fn_off, const int32_t* par_off,
 {
     if (init && step0 != 0)
         return 2;
-    oracle_model m = {n, fn_off, par_off, parents, tbl_off, tables, sel_prob, p, per_node};
+    /* per_node: 0 VECTOR, 1 PER_NODE, 2 VECTOR with the geometric-skip stream */
+    const int geometric = per_node == 2;
+    oracle_model m = {n, fn_off, par_off, parents, tbl_off, tables, sel_prob, p, geometric ? 0 : per_node};
     uint64_t* D = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(fn_off[n] > 0 ? fn_off[n] : 1));
     uint32_t* u = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
     uint8_t* s_next = (uint8_t*)malloc((size_t)n);
-    if (!D || !u || !s_next) {
-        free(D); free(u); free(s_next);
+    uint32_t* Cg = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
+    uint8_t* gam = (uint8_t*)malloc((size_t)n);
+    if (!D || !u || !s_next || !Cg || !gam) {
+        free(D); free(u); free(s_next); free(Cg); free(gam);
         return 1;
     }
-    oracle_selection_thresholds(n, fn_off, sel_prob, p, D);
+    /* geometric mode: selection thresholds with no perturbation share (T_p = 0) */
+    oracle_selection_thresholds(n, fn_off, sel_prob, geometric ? 0.0 : p, D);
     uint32_t Tp = oracle_perturbation_threshold(p);
+    if (geometric)
+        oracle_geometric_table(n, p, Cg);
 
     for (int64_t c = 0; c < nchains; ++c) {
         uint32_t chain = chain_ids[c];
@@ -231,7 +300,16 @@ int oracle_simulate(int32_t n, const int32_t* fn_off, const int32_t* par_off,
             uint64_t t = (uint64_t)(step0 + r);
             for (int32_t i = 0; i < n; ++i)
                 u[i] = oracle_word(seed, chain, t, (uint32_t)i);
-            step_with_words(&m, Tp, D, s, u, s_next);
+            if (geometric) {
+                if (geometric_gamma(Cg, n, seed, chain, t, gam) > 0) {
+                    for (int32_t i = 0; i < n; ++i) /* s(t+1) = s(t) XOR gamma(t) */
+                        s_next[i] = (uint8_t)(s[i] ^ gam[i]);
+                } else {
+                    step_with_words(&m, 0u, D, s, u, s_next); /* no perturbation: f(t)(s(t)) */
+                }
+            } else {
+                step_with_words(&m, Tp, D, s, u, s_next);
+            }
             memcpy(s, s_next, (size_t)n);
             if (r > burn_in) {
                 int I = 1;
@@ -242,6 +320,6 @@ int oracle_simulate(int32_t n, const int32_t* fn_off, const int32_t* par_off,
             }
         }
     }
-    free(D); free(u); free(s_next);
+    free(D); free(u); free(s_next); free(Cg); free(gam);
     return 0;
 }

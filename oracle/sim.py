@@ -49,6 +49,12 @@ def lib():
                 C.c_int64, C.c_int32, C.c_int32, _p(np.uint16, flags="C"),
                 _p(np.uint8, flags="C"), _p(np.uint8, flags="C"), _p(np.uint8, flags="C")]
             L.oracle_simulate.restype = C.c_int
+            L.oracle_geometric_table.argtypes = [C.c_int32, C.c_double, _p(np.uint32, flags="C")]
+            L.oracle_geometric_table.restype = None
+            L.oracle_skip_word.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32]
+            L.oracle_skip_word.restype = C.c_uint32
+            L.oracle_skip.argtypes = [_p(np.uint32, flags="C"), C.c_int32, C.c_uint32]
+            L.oracle_skip.restype = C.c_int32
             _lib = L
     return _lib
 
@@ -95,12 +101,30 @@ def step(model, s, u, per_node: bool = False) -> np.ndarray:
     return out
 
 
+def geometric_table(model) -> np.ndarray:
+    Cg = np.zeros(max(int(model.n), 1), np.uint32)
+    lib().oracle_geometric_table(int(model.n), float(model.p), Cg)
+    return Cg[:model.n]
+
+
+def skip_word(seed: int, chain: int, t: int, m: int) -> int:
+    return int(lib().oracle_skip_word(seed, chain, t, m))
+
+
+def skip(Cg: np.ndarray, v: int) -> int:
+    Cg = np.ascontiguousarray(Cg, np.uint32)
+    return int(lib().oracle_skip(Cg, len(Cg), int(v)))
+
+
 def simulate(model, pred, seed: int, chain_ids, step0: int, burn_in: int, steps: int,
-             init: bool = True, state=None, per_node: bool = False, threads: int = 1):
+             init: bool = True, state=None, per_node: bool = False, threads: int = 1,
+             geometric: bool = False):
     """Run the oracle trajectories.
 
     Returns (state [nchains x n] uint8 = s_{step0+burn_in+steps},
              I [nchains x steps] uint8 = indicator over the recorded window).
+    geometric: VECTOR semantics with the geometric-skip perturbation stream
+    (NEXT-2, reading Q18).
     With threads > 1 the chain list is split over a thread pool (the C call
     releases the GIL); results do not depend on the split.
     """
@@ -113,7 +137,9 @@ def simulate(model, pred, seed: int, chain_ids, step0: int, burn_in: int, steps:
     else:
         st = np.array(state, dtype=np.uint8, copy=True).reshape(nch, n)
     I = np.zeros((nch, max(steps, 0)), np.uint8)
-    margs = _model_args(model, per_node)
+    if geometric and per_node:
+        raise ValueError("the geometric-skip stream is defined for VECTOR semantics (reading Q18)")
+    margs = _model_args(model, 2 if geometric else per_node)
     pn = np.ascontiguousarray(pred.nodes, np.uint16) if pred.k else np.zeros(1, np.uint16)
     pv = np.ascontiguousarray(pred.values, np.uint8) if pred.k else np.zeros(1, np.uint8)
 
