@@ -37,7 +37,7 @@ UNIT = "node-updates/s"
 SM_COUNT_B200 = 148
 
 
-def demand_per_node_update(model) -> dict:
+def demand_per_node_update(model, geometric: bool = False) -> dict:
     """Algorithmic demand per node-update, SURVEY §8(d) (declared from the
     method and the one-word-per-node-update stream of reading Q3, not from the
     achieved SASS), averaged over the nodes:
@@ -54,7 +54,13 @@ def demand_per_node_update(model) -> dict:
     lane the binary search's thresholds (4 B per step), the selected
     function's descriptor (16 B), its parent offsets (4 B each) and one
     table word (4 B); the node record (16 B) is shared by the 32 lanes.
-    theta_sel, [theta >= 6] are weighted by the selection probabilities."""
+    theta_sel, [theta >= 6] are weighted by the selection probabilities.
+
+    geometric (NEXT-2, reading Q18): gamma(t) comes from the skip stream, so
+    a node-update needs a selection word only when its node has ell > 1, no
+    T_p compare, and under VECTOR no evaluation at all on the chain-steps
+    with gamma != 0: every node term is scaled by P(gamma = 0) = (1-p)^n
+    (the skip draws cost ~(1 + n p) words per chain-step, / n per node)."""
     ell = np.diff(model.fn_off).astype(np.float64)
     theta = np.diff(model.par_off).astype(np.float64)
     node_of_fn = np.repeat(np.arange(model.n), np.diff(model.fn_off))
@@ -67,6 +73,12 @@ def demand_per_node_update(model) -> dict:
     decide = np.where(slow, 1.0 + 3.0 * steps, ell + 1.0)
     alu = (5.0 + decide + 2.0 * sel_theta + 2.0 + sel_big + 1.0).mean()
     fma = 5.0
+    if geometric:
+        p0 = (1.0 - float(model.p)) ** model.n
+        needs_word = (ell > 1).astype(np.float64)
+        alu = float(p0 * (5.0 * needs_word + (decide - 1.0) + 2.0 * sel_theta + 2.0 + sel_big + 1.0).mean())
+        fma = float(p0 * 5.0 * needs_word.mean())
+        sel_theta = p0 * (sel_theta + 1.0) - 1.0      # smem demand below: p0 (theta_sel + 1) / 32
     img_bytes = np.where(slow, 16.0 / 32 + 4.0 * steps + 16.0 + 4.0 * sel_theta + 4.0, 0.0).mean()
     return {"alu": float(alu), "fma": fma, "issue": float(alu + fma),
             "lds_wavefronts": float((sel_theta.mean() + 1.0) / 32.0), "image_bytes": float(img_bytes),
@@ -93,11 +105,11 @@ def load_peaks() -> dict:
             "l2_read_gbs": None}
 
 
-def roofline(model, node_updates: float, kernel_s: float, sm_mhz: float) -> dict:
+def roofline(model, node_updates: float, kernel_s: float, sm_mhz: float, geometric: bool = False) -> dict:
     """Roofline of K1 in node-updates/s = min over resources of peak/demand
     (SURVEY §8(d)); frac = achieved / roofline; `achieved`/`peak` are given
     in the binding resource's unit (T ops/s or T wavefronts/s)."""
-    d = demand_per_node_update(model)
+    d = demand_per_node_update(model, geometric)
     pk = load_peaks()
     hz = sm_mhz * 1e6 * SM_COUNT_B200
     res = {
@@ -245,7 +257,8 @@ def workload_config(args, cfg, model) -> dict:
         "chains_per_gpu": args.chains, "burn_in": args.burn_in, "window": args.window,
         "batch": cfg.batch, "n": model.n, "functions": int(model.nf),
         "density": float(model.par_off[-1]) / model.n, "seed": cfg.sim_seed,
-        "semantics": "VECTOR", "l2": "256 MiB buffer written between timed steps",
+        "semantics": "VECTOR, geometric-skip stream (NEXT-2)" if getattr(args, "geometric", False) else "VECTOR",
+        "l2": "256 MiB buffer written between timed steps",
     }
 
 
@@ -311,6 +324,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
     ap.add_argument("--sweep", action="store_true", help="C5 chain-count sweep (one line per count)")
     ap.add_argument("--e2e-steps", type=int, default=3, help="timed end-to-end (host buffer) iterations")
+    ap.add_argument("--geometric", action="store_true",
+                    help="geometric-skip perturbation stream (NEXT-2, PBN_PERTURB_GEOMETRIC)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
@@ -343,7 +358,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    pm = pbn.pbn_load(model)
+    pm = pbn.pbn_load(model, geometric=args.geometric)
     chains, burn_in, window, batch = args.chains, args.burn_in, args.window, cfg.batch
     chain_base = rank * chains                    # disjoint global chain ids per rank
     out = pbn.alloc_outputs(pm, chains, window, batch=batch, emit_bits=True)
@@ -403,7 +418,7 @@ def main():
                 sm_mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
         except Exception:
             sm_mhz = 1965.0
-    rf = roofline(model, node_updates_per_step, avg_kernel_s, sm_mhz)
+    rf = roofline(model, node_updates_per_step, avg_kernel_s, sm_mhz, args.geometric)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_C4.json")
     if os.path.exists(tpath):

@@ -42,7 +42,17 @@ typedef enum {
 /* Perturbation semantics (reading Q1), chosen at load time. */
 enum {
     PBN_PERTURB_VECTOR = 0,   /* any gamma_i(t)=1  =>  s(t+1) = s(t) XOR gamma(t) */
-    PBN_PERTURB_PER_NODE = 1  /* node i flips iff gamma_i(t)=1, else applies f     */
+    PBN_PERTURB_PER_NODE = 1, /* node i flips iff gamma_i(t)=1, else applies f     */
+    /* VECTOR semantics with gamma(t) drawn by geometric skips from its own word
+     * stream (SPEC S:177's optional mode, reading Q18):
+     *   k_1 = G(v_0), k_{j+1} = k_j + 1 + G(v_j) until k >= n, gamma_k = 1,
+     *   G(v) = #{g < n : Cg[g] <= v}, Cg[g] = floor((1 - q^(g+1)) 2^32),
+     *   q = 1 - p (q^(g+1) by repeated fp64 multiplication),
+     *   v(chain,t,m) = Philox4x32-10((2^31 + m/4, chain, t mod 2^32, t >> 32), key)[m mod 4];
+     * with gamma(t) = 0 node i selects with its word u(chain,t,i) against the
+     * unperturbed thresholds Q_j (T_p = 0).  A different random stream from
+     * VECTOR's (same law up to the 2^-32 quantisation). */
+    PBN_PERTURB_GEOMETRIC = 2
 };
 
 /* -------------------------------------------------------------------- */

@@ -31,6 +31,7 @@ STATUS_NAMES = {0: "PBN_OK", 1: "PBN_E_INVALID", 2: "PBN_E_USAGE", 3: "PBN_E_DEG
 
 PBN_PERTURB_VECTOR = 0
 PBN_PERTURB_PER_NODE = 1
+PBN_PERTURB_GEOMETRIC = 2
 PBN_LAYOUT_AUTO = 0
 PBN_LAYOUT_CHAIN_LANES = 1
 PBN_LAYOUT_NODE_LANES = 2

@@ -19,7 +19,7 @@ __all__ = ["Model", "SimOutputs", "pbn_load", "pbn_validate", "pbn_simulate", "p
            "pbn_skart_ci_from_batches", "pbn_skart", "pbn_run", "pbn_version", "alloc_outputs", "PbnError"]
 
 
-def _desc(m, per_node: bool):
+def _desc(m, per_node: bool, geometric: bool = False):
     """Build a pbn_model_desc from an object carrying the CSR arrays
     (workloads.PbnModel or anything with the same attribute names)."""
     keep = dict(
@@ -43,7 +43,8 @@ def _desc(m, per_node: bool):
         tables=L._ptr(keep["tables"], C.c_uint32),
         sel_prob=L._ptr(keep["sel_prob"], C.c_double),
         p=float(m.p),
-        flags=L.PBN_PERTURB_PER_NODE if per_node else L.PBN_PERTURB_VECTOR,
+        flags=(L.PBN_PERTURB_GEOMETRIC if geometric else
+               L.PBN_PERTURB_PER_NODE if per_node else L.PBN_PERTURB_VECTOR),
     )
     return d, keep
 
@@ -83,8 +84,12 @@ class Model:
             pass
 
 
-def pbn_load(model, per_node: bool = False, device: int = -1) -> Model:
-    d, _keep = _desc(model, per_node)
+def pbn_load(model, per_node: bool = False, device: int = -1, geometric: bool = False) -> Model:
+    """geometric: VECTOR semantics with the geometric-skip perturbation stream
+    (PBN_PERTURB_GEOMETRIC, NEXT-2, reading Q18)."""
+    if geometric and per_node:
+        raise ValueError("the geometric-skip stream is defined for VECTOR semantics")
+    d, _keep = _desc(model, per_node, geometric)
     h = C.c_void_p()
     err = C.create_string_buffer(512)
     check(lib().pbn_load(C.byref(d), int(device), C.byref(h), err, 512), err.value)

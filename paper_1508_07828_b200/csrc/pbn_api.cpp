@@ -98,8 +98,8 @@ pbn_status validate(const pbn_model_desc* d, char* err, size_t errlen)
         set_err(err, errlen, "perturbation p must satisfy 2^-32 <= p < 1 (got %.17g)", d->p);
         return PBN_E_INVALID;
     }
-    if (d->flags > PBN_PERTURB_PER_NODE) {
-        set_err(err, errlen, "unknown flags %u", d->flags);
+    if (d->flags > PBN_PERTURB_GEOMETRIC) {
+        set_err(err, errlen, "unknown flags %u (VECTOR, PER_NODE or GEOMETRIC)", d->flags);
         return PBN_E_INVALID;
     }
     if (d->fn_off[0] != 0) {
@@ -222,7 +222,8 @@ inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
 // 48: three buffers, pbn_cluster).  The fast width FT and the slow-node
 // count are model-wide, so every sub-image of a cluster uses one kernel.
 std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L, int32_t node_lo = 0,
-                                 int32_t node_hi = -1, uint32_t qs = 32, bool packed = false)
+                                 int32_t node_hi = -1, uint32_t qs = 32, bool packed = false, bool geo = false,
+                                 double geo_p = 0.0)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
     if (node_hi < 0) node_hi = n;
@@ -338,6 +339,16 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
         rec[3] = w3;
         reloc.push_back(off_nrec + 16u * (uint32_t)(i - node_lo) + 12u);
     }
+    if (geo) {
+        // geometric-skip table Cg[g] = floor((1 - q^(g+1)) 2^32), q^(g+1) by
+        // repeated fp64 multiplication (reading Q18)
+        L->geo_off = B.alloc(4u * (size_t)n, 16);
+        double q = 1.0 - geo_p, r = 1.0;
+        for (int32_t g = 0; g < n; ++g) {
+            r *= q;
+            B.u32(L->geo_off)[g] = (uint32_t)std::floor(std::ldexp(1.0 - r, 32));
+        }
+    }
     B.alloc(16);  // tail slack
     L->bytes = (uint32_t)B.buf.size();
     // relocation list after the image (not staged to shared memory)
@@ -394,7 +405,10 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     m->flags = desc->flags;
     m->Tp = quantise_p(desc->p);
     m->n_parents = desc->par_off[desc->fn_off[desc->n]];
-    std::vector<uint8_t> img = build_image(desc, m->Tp, &m->L);
+    const bool geo = desc->flags == PBN_PERTURB_GEOMETRIC;
+    // geometric mode: no per-node perturbation share in the thresholds (T_p = 0)
+    const uint32_t Tsel = geo ? 0u : m->Tp;
+    std::vector<uint8_t> img = build_image(desc, Tsel, &m->L, 0, -1, 32u, false, geo, desc->p);
     e = cudaMalloc(&m->d_image, img.size());
     if (e != cudaSuccess) {
         delete m;
@@ -409,7 +423,9 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     // sub-images for the cluster kernel: CTA r of a K-cluster owns quads
     // [Q r / K, Q (r+1) / K) and its nodes' records and descriptors
     const int32_t nq = (desc->n + 3) / 4;
-    for (int K = 2; K <= pbn::kMaxCluster && K <= nq; K *= 2) {
+    // the geometric-skip stream runs in K1 (the cluster and lanes-over-nodes
+    // kernels draw gamma per node): no sub-images for it
+    for (int K = 2; !geo && K <= pbn::kMaxCluster && K <= nq; K *= 2) {
         ClusterImages ci;
         ci.K = K;
         std::vector<uint8_t> all;
@@ -441,7 +457,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     // packed sub-images for the lanes-over-nodes kernel: CTA r of a K-cluster
     // owns packed state words [W r / K, W (r+1) / K)
     const int32_t nw = (desc->n + 31) / 32;
-    for (int K = 1; K <= pbn::kMaxCluster && K <= nw; K *= 2) {
+    for (int K = 1; !geo && K <= pbn::kMaxCluster && K <= nw; K *= 2) {
         NodeParImages ni;
         ni.K = K;
         std::vector<uint8_t> all;
@@ -523,8 +539,10 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     std::memset(P, 0, sizeof(*P));
     P->image = m->d_image;
     P->L = m->L;
-    P->Tp = m->Tp;
     P->per_node = m->flags == PBN_PERTURB_PER_NODE;
+    P->geometric = m->flags == PBN_PERTURB_GEOMETRIC ? 1 : 0;
+    // geometric mode: gamma comes from the skip stream, never from u < T_p
+    P->Tp = P->geometric ? 0u : m->Tp;
     P->n = m->L.n;
     P->nquads = (m->L.n + 3) / 4;
     P->n_pad = (m->L.n + 3) & ~3;

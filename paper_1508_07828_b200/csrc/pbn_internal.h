@@ -95,14 +95,16 @@ struct ImageLayout {
     int32_t max_theta = 0, max_ell = 0;
     int32_t slow_nodes = 0;
     int32_t fast_theta = kFastMinTheta;  // FT
+    uint32_t geo_off = 0;      // geometric-skip table Cg[0..n-1] (u32), PBN_PERTURB_GEOMETRIC only
 };
 
 struct TrajParams {
     const uint8_t* image;      // device image (global); relocation list at image + L.reloc_off
     ImageLayout L;
     uint32_t rk[20];           // Philox round keys (k0 + r W0, k1 + r W1), r = 0..9
-    uint32_t Tp;
+    uint32_t Tp;               // perturbation threshold of the node words (0 in geometric mode)
     int32_t per_node;          // PBN_PERTURB_PER_NODE semantics
+    int32_t geometric;         // PBN_PERTURB_GEOMETRIC: gamma(t) from the skip stream (reading Q18)
     int32_t n;
     int32_t nquads;            // ceil(n/4)
     int32_t n_pad;             // n rounded up to a multiple of 4 (u32 words per buffer)

@@ -250,6 +250,12 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
         const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
         uint32_t any = 0;
         const PhiloxStep ps = philox_step(chain, t_lo, t_hi, P.rk);
+        // geometric-skip stream (reading Q18): warp 0 draws every lane's
+        // gamma(t) and marks it in the gamma words; the VECTOR fix-up after
+        // the step barrier applies it (the node words carry no perturbation)
+        if (!PER_NODE && P.geometric && wg == 0)
+            any |= geometric_gamma(img, (SMEM ? sbase : 0u) + P.L.geo_off, n, chain, t_lo, t_hi, P.rk, gam, lmask,
+                                   valid);
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)

@@ -71,10 +71,10 @@ def gpu_run(pm, model, pred, *, n_chains, steps, burn_in=0, step0=0, chain_base=
 
 
 def oracle_run(model, pred, chain_ids, *, steps, burn_in=0, step0=0, seed=1, batch=0, init=True,
-               state=None, per_node=False, threads=8):
+               state=None, per_node=False, threads=8, geometric=False):
     st, I = osim.simulate(model, pred, seed=seed, chain_ids=np.asarray(chain_ids, np.uint32),
                           step0=step0, burn_in=burn_in, steps=steps, init=init, state=state,
-                          per_node=per_node, threads=threads)
+                          per_node=per_node, threads=threads, geometric=geometric)
     ws = [ostats.window_stats(I[c], batch if batch > 0 else max(steps, 1)) for c in range(len(chain_ids))]
     return st, I, ws
 

@@ -515,3 +515,62 @@ def test_dense_small_model_every_kernel(pbn, per_node, monkeypatch):
     monkeypatch.delenv("PBN_FORCE_GLOBAL_IMAGE")
     for c in range(40):
         compare_chain(g, c, packed[c], ws[c], 500, 25)
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: the geometric-skip perturbation stream (PBN_PERTURB_GEOMETRIC,
+# reading Q18; oracle pinned in test_oracle_geometric.py)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("key,chains", [("C1", 4), ("C2", 200), ("C3", 64)])
+def test_geometric_mode_all_chains(pbn, key, chains):
+    c = CONFIGS[key]
+    model, pred = config_model(key), config_predicate(key)
+    pm = pbn.pbn_load(model, geometric=True)
+    steps, burn_in = min(c.steps, 3000), min(c.burn_in, 500)
+    g = gpu_run(pm, model, pred, n_chains=chains, steps=steps, burn_in=burn_in, seed=c.sim_seed, batch=c.batch)
+    st, I, ws = oracle_run(model, pred, np.arange(chains), steps=steps, burn_in=burn_in, seed=c.sim_seed,
+                           batch=c.batch, geometric=True, threads=os.cpu_count() or 8)
+    packed = pack_states(st)
+    for j in range(chains):
+        compare_chain(g, j, packed[j], ws[j], steps, c.batch)
+    assert np.array_equal(g["totals"], ostats.totals(ws))
+
+
+def test_geometric_mode_C4_sampled_chains_and_launch_shapes(pbn):
+    """C4 at its full size with the geometric stream (persistent schedule),
+    sampled chains vs the oracle; plus launch-shape independence (warps,
+    persistent chunks, global image) on a ragged chain count."""
+    c = CONFIGS["C4"]
+    model, pred = config_model("C4"), config_predicate("C4")
+    pm = pbn.pbn_load(model, geometric=True)
+    g = gpu_run(pm, model, pred, n_chains=c.chains, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch)
+    ids = sample_chain_ids(c.chains, k=24, seed=c.sim_seed)
+    st, I, ws = oracle_run(model, pred, ids, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch,
+                           geometric=True, threads=os.cpu_count() or 8)
+    packed = pack_states(st)
+    for k, cid in enumerate(ids):
+        compare_chain(g, cid, packed[k], ws[k], c.steps, c.batch)
+    kw = dict(n_chains=1000, steps=300, burn_in=40, seed=3, batch=30)
+    ref = gpu_run(pm, model, pred, schedule=1, **kw)
+    for extra in [dict(warps=7, schedule=1), dict(schedule=2, chunk_steps=17), dict(schedule=0)]:
+        b = gpu_run(pm, model, pred, **kw, **extra)
+        for k in ALL:
+            assert np.array_equal(ref[k], b[k]), (extra, k)
+    import os as _os
+    _os.environ["PBN_FORCE_GLOBAL_IMAGE"] = "1"
+    try:
+        b = gpu_run(pm, model, pred, schedule=1, **kw)
+    finally:
+        del _os.environ["PBN_FORCE_GLOBAL_IMAGE"]
+    for k in ALL:
+        assert np.array_equal(ref[k], b[k]), ("global image", k)
+
+
+def test_geometric_mode_rejects_other_kernels(pbn):
+    import paper_1508_07828_b200 as P
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = pbn.pbn_load(model, geometric=True)
+    with pytest.raises(P.PbnError):
+        gpu_run(pm, model, pred, n_chains=40, steps=10, cluster_size=2)
+    with pytest.raises(P.PbnError):
+        gpu_run(pm, model, pred, n_chains=40, steps=10, layout=NODE_LANES)
