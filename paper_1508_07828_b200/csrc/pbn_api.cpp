@@ -223,7 +223,7 @@ inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
 // count are model-wide, so every sub-image of a cluster uses one kernel.
 std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L, int32_t node_lo = 0,
                                  int32_t node_hi = -1, uint32_t qs = 32, bool packed = false, bool geo = false,
-                                 double geo_p = 0.0)
+                                 double geo_p = 0.0, bool skew = false)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
     if (node_hi < 0) node_hi = n;
@@ -263,6 +263,16 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
         if (fast[i]) {
             const int32_t tm = FT;  // every fast function is padded to the model-wide FT
             const uint32_t ds = pbn::desc_bytes(tm);
+            if (packed && skew) {
+                // lanes over nodes: the 32 lanes of a warp read the selected
+                // descriptors of 32 consecutive nodes; skew each node's block
+                // to start at 16 (i mod 8) modulo 128 bytes so those 16-byte
+                // chunks spread over all 32 banks (C5 K1n: an LDS.128 of
+                // descriptors cost 19.8 wavefronts with 64-byte-aligned blocks)
+                // -- at up to 112 padding bytes per node
+                const size_t want = 16u * (size_t)(i & 7);
+                while ((B.buf.size() & 127u) != want) B.alloc(16, 16);
+            }
             const uint32_t off_desc = B.alloc((size_t)ds * ell, 16);
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;
@@ -286,6 +296,17 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                     }
                     // stored bit-reversed per word: entry e at bit 31 - (e & 31)
                     for (size_t q = 0; q < T.size(); ++q) w[8 + q] = reverse_bits(T[q]);
+                    if (packed && tm == 8) {
+                        // lanes over nodes: XOR-swizzle the 4 16-byte chunks by the
+                        // descriptor's own 64-byte index (mod 4) so that the
+                        // selected descriptors of 32 consecutive nodes spread
+                        // over the banks (fast_bit_packed<8> undoes it)
+                        const uint32_t sw = (wbase >> 6) & 3u;
+                        uint32_t logical[16];
+                        for (int q = 0; q < 16; ++q) logical[q] = w[q];
+                        for (uint32_t c = 0; c < 4; ++c)
+                            for (uint32_t k = 0; k < 4; ++k) w[4u * (c ^ sw) + k] = logical[4u * c + k];
+                    }
                 } else {
                     int k = 0;
                     w[k++] = reverse_bits(T[0]);
@@ -457,15 +478,31 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     // packed sub-images for the lanes-over-nodes kernel: CTA r of a K-cluster
     // owns packed state words [W r / K, W (r+1) / K)
     const int32_t nw = (desc->n + 31) / 32;
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     for (int K = 1; !geo && K <= pbn::kMaxCluster && K <= nw; K *= 2) {
         NodeParImages ni;
         ni.K = K;
         std::vector<uint8_t> all;
         for (int r = 0; r <= K; ++r) ni.w_lo[r] = (int32_t)((int64_t)nw * r / K);
+        // skewed descriptor blocks when the padded sub-images still fit one
+        // CTA's shared memory, else the compact layout (C5: K = 4 fits only
+        // compact, and K = 4 is its fastest 64-chain cluster size)
+        bool skew = true;
+        {
+            uint32_t mx = 0;
+            for (int r = 0; r < K; ++r) {
+                pbn::ImageLayout Lr;
+                build_image(desc, m->Tp, &Lr, 32 * ni.w_lo[r], std::min(desc->n, 32 * ni.w_lo[r + 1]), 32u, true,
+                            false, 0.0, true);
+                mx = std::max(mx, Lr.bytes);
+            }
+            skew = pbn::nodepar_smem_bytes(nw, 1, mx) + 64 <= (size_t)smem_optin;
+        }
         for (int r = 0; r < K; ++r) {
             pbn::ImageLayout Lr;
             const int32_t lo = 32 * ni.w_lo[r], hi = std::min(desc->n, 32 * ni.w_lo[r + 1]);
-            std::vector<uint8_t> sub = build_image(desc, m->Tp, &Lr, lo, hi, 32u, true);
+            std::vector<uint8_t> sub = build_image(desc, m->Tp, &Lr, lo, hi, 32u, true, false, 0.0, skew);
             const size_t off = (all.size() + 15) & ~(size_t)15;
             all.resize(off + sub.size(), 0);
             std::memcpy(all.data() + off, sub.data(), sub.size());

@@ -106,19 +106,23 @@ __device__ __forceinline__ uint32_t pbit(uint32_t S, uint32_t p)
 // A6 for one fast function of the packed image: descriptor at dp, parents
 // are node ids, MSB first (reading Q5); returns the new bit
 template <int FT>
-__device__ __forceinline__ uint32_t fast_bit_packed(uint32_t dp, uint32_t S)
+__device__ __forceinline__ uint32_t fast_bit_packed(uint32_t dp, uint32_t S, uint32_t ibase)
 {
     uint32_t tw, idx = 0;
     if constexpr (FT >= 7) {
-        // {a[0..7], table words}: the first FT-5 parents pick the table word
-        const uint4 d0 = lds128_ro(dp), d1 = lds128_ro(dp + 16u);
+        // {a[0..7], table words}: the first FT-5 parents pick the table word;
+        // FT = 8: 16-byte chunk c stored at chunk c ^ sw, sw = the descriptor's
+        // 64-byte index mod 4 within the sub-image (bank spread, build_image)
+        const uint32_t sw = FT == 8 ? ((dp - ibase) >> 6) & 3u : 0u;
+        const uint4 d0 = lds128_ro(dp + 16u * (0u ^ sw)), d1 = lds128_ro(dp + 16u * (1u ^ sw));
         const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
         uint32_t widx = 0;
 #pragma unroll
         for (int m = 0; m < FT - 5; ++m) widx = 2u * widx + pbit(S, a[m]);
 #pragma unroll
         for (int m = FT - 5; m < FT; ++m) idx = 2u * idx + pbit(S, a[m]);
-        tw = lds32_ro(dp + 32u + 4u * widx);
+        tw = FT == 8 ? lds32_ro(dp + 16u * ((2u + (widx >> 2)) ^ sw) + 4u * (widx & 3u))
+                     : lds32_ro(dp + 32u + 4u * widx);
     } else {
         // {t0, [t1], a[0..FT-1]}
         const uint4 d0 = lds128_ro(dp);
@@ -267,8 +271,15 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
         const uint32_t bar = par ? bx1 : bx0;
         const uint64_t t = (uint64_t)(P.step0 + r);
         // ---- A3-A6: warp = (chain g, own word j), lane = node 32 j + lane ----
-        for (int it = wg; it < Ge * OW; it += NWARP) {
-            const int g = it / OW, j = w_lo + it % OW;
+        // (items it = g OW + (j - w_lo) strided by the warp count, walked
+        // without integer division)
+        int g = wg / OW, jj = wg % OW;
+        for (int it = wg; it < Ge * OW; it += NWARP, jj += NWARP) {
+            while (jj >= OW) {
+                jj -= OW;
+                ++g;
+            }
+            const int j = w_lo + jj;
             const uint32_t chain = (uint32_t)(P.chain_base + chain0 + g);
             const uint32_t So = Sp(par ^ 1u, g);
             const uint32_t i = 32u * (uint32_t)j + (uint32_t)lane;
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
                 if (u > rec.x) dp += DS;
                 if (u > rec.y) dp += DS;
                 if (u > rec.z) dp += DS;
-                bit = fast_bit_packed<FT>(dp, So);
+                bit = fast_bit_packed<FT>(dp, So, ibase);
             } else {
                 bit = slow_bit_packed(rec.w, u, So);
             }
@@ -301,8 +312,10 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
             if (lane < (int)K && lane != (int)rank)
                 st_async_v2(np_map_peer(a, (uint32_t)lane), vf, vg, np_map_peer(bar, (uint32_t)lane));
         }
-        // ---- wait for every peer's words of this step ----
-        mbar_wait(bar, (uint32_t)((r - 1) >> 1) & 1u);
+        // ---- wait for every peer's words of this step: one warp spins on the
+        // mbarrier, the others wait in the CTA barrier (spinning warps would
+        // steal issue slots from the warps still computing) ----
+        if (wg == 0) mbar_wait(bar, (uint32_t)((r - 1) >> 1) & 1u);
         __syncthreads();  // this CTA's own words too
         // ---- A7 commit of every chain (VECTOR: any gamma -> s XOR gamma), warp per chain ----
         for (int g = wg; g < Ge; g += NWARP) {
