@@ -45,6 +45,8 @@ struct pbn_model_s {
     int64_t n_parents = 0;
     std::vector<ClusterImages> clusters;  // K = 2, 4, 8, 16 (K <= quads)
     std::vector<NodeParImages> nodepar;   // K = 1, 2, 4, 8, 16 (K <= packed words)
+    uint32_t geo_last = 0;                // geometric mode: Cg[n-1]
+    double p = 0.0;
 };
 
 namespace {
@@ -425,11 +427,13 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     m->device = device;
     m->flags = desc->flags;
     m->Tp = quantise_p(desc->p);
+    m->p = desc->p;
     m->n_parents = desc->par_off[desc->fn_off[desc->n]];
     const bool geo = desc->flags == PBN_PERTURB_GEOMETRIC;
     // geometric mode: no per-node perturbation share in the thresholds (T_p = 0)
     const uint32_t Tsel = geo ? 0u : m->Tp;
     std::vector<uint8_t> img = build_image(desc, Tsel, &m->L, 0, -1, 32u, false, geo, desc->p);
+    if (geo) std::memcpy(&m->geo_last, img.data() + m->L.geo_off + 4u * (uint32_t)(desc->n - 1), 4);
     e = cudaMalloc(&m->d_image, img.size());
     if (e != cudaSuccess) {
         delete m;
@@ -480,7 +484,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     const int32_t nw = (desc->n + 31) / 32;
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    for (int K = 1; !geo && K <= pbn::kMaxCluster && K <= nw; K *= 2) {
+    for (int K = 1; K <= pbn::kMaxCluster && K <= nw; K *= 2) {
         NodeParImages ni;
         ni.K = K;
         std::vector<uint8_t> all;
@@ -493,7 +497,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
             uint32_t mx = 0;
             for (int r = 0; r < K; ++r) {
                 pbn::ImageLayout Lr;
-                build_image(desc, m->Tp, &Lr, 32 * ni.w_lo[r], std::min(desc->n, 32 * ni.w_lo[r + 1]), 32u, true,
+                build_image(desc, Tsel, &Lr, 32 * ni.w_lo[r], std::min(desc->n, 32 * ni.w_lo[r + 1]), 32u, true,
                             false, 0.0, true);
                 mx = std::max(mx, Lr.bytes);
             }
@@ -502,7 +506,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
         for (int r = 0; r < K; ++r) {
             pbn::ImageLayout Lr;
             const int32_t lo = 32 * ni.w_lo[r], hi = std::min(desc->n, 32 * ni.w_lo[r + 1]);
-            std::vector<uint8_t> sub = build_image(desc, m->Tp, &Lr, lo, hi, 32u, true, false, 0.0, skew);
+            std::vector<uint8_t> sub = build_image(desc, Tsel, &Lr, lo, hi, 32u, true, false, 0.0, skew);
             const size_t off = (all.size() + 15) & ~(size_t)15;
             all.resize(off + sub.size(), 0);
             std::memcpy(all.data() + off, sub.data(), sub.size());
@@ -580,6 +584,7 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     P->geometric = m->flags == PBN_PERTURB_GEOMETRIC ? 1 : 0;
     // geometric mode: gamma comes from the skip stream, never from u < T_p
     P->Tp = P->geometric ? 0u : m->Tp;
+    P->geo_inv_lnq = P->geometric ? (float)(1.0 / std::log1p(-m->p)) : 0.0f;
     P->n = m->L.n;
     P->nquads = (m->L.n + 3) / 4;
     P->n_pad = (m->L.n + 3) & ~3;
@@ -695,6 +700,10 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         C.T.image = np_use->d_buf;
         C.K = np_use->K;
         C.G = np_G(*np_use);
+        if (P.geometric) {
+            C.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->L.geo_off);
+            C.geo_last = m->geo_last;
+        }
         if (a->chains_per_cluster > 0 && C.G != a->chains_per_cluster) return PBN_E_USAGE;
         C.n_words = nw;
         int ow = 0;
@@ -706,8 +715,9 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
             ow = std::max(ow, np_use->w_lo[r + 1] - np_use->w_lo[r]);
         }
         for (int r = 0; r <= np_use->K; ++r) C.w_lo[r] = np_use->w_lo[r];
-        // one warp per (chain, own word) -- up to 32 warps, which then loop
-        int threads = std::min(1024, 32 * C.G * ow);
+        // one warp per (chain, own word) -- up to 32 warps, which then loop;
+        // the geometric stream adds a warp that only draws gamma(t+1)
+        int threads = std::min(1024, 32 * (C.G * ow + (P.geometric ? 1 : 0)));
         if (a->warps_per_group > 0) threads = std::min(1024, 32 * a->warps_per_group);
         threads = std::max(threads, 32 * P.n_props);
         const size_t smem = pbn::nodepar_smem_bytes(nw, C.G, np_use->max_bytes);

@@ -105,6 +105,7 @@ struct TrajParams {
     uint32_t Tp;               // perturbation threshold of the node words (0 in geometric mode)
     int32_t per_node;          // PBN_PERTURB_PER_NODE semantics
     int32_t geometric;         // PBN_PERTURB_GEOMETRIC: gamma(t) from the skip stream (reading Q18)
+    float geo_inv_lnq;         // 1 / ln(1 - p): start of the skip search (the table decides)
     int32_t n;
     int32_t nquads;            // ceil(n/4)
     int32_t n_pad;             // n rounded up to a multiple of 4 (u32 words per buffer)
@@ -174,6 +175,8 @@ struct NodeParParams {
     uint32_t reloc_off[kMaxCluster];
     int32_t reloc_count[kMaxCluster];
     int32_t w_lo[kMaxCluster + 1];
+    const uint32_t* geo_table;  // geometric mode: Cg[0..n-1] in global memory (the full image's copy)
+    uint32_t geo_last;          // Cg[n-1]: gamma(t) != 0 iff the first skip word is below it
 };
 size_t nodepar_smem_bytes(int n_words, int G, uint32_t max_sub_image);
 int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, void* stream);

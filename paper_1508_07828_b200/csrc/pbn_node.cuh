@@ -350,16 +350,17 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, const uint4 
 
 // Geometric-skip perturbation stream (PBN_PERTURB_GEOMETRIC, reading Q18),
 // one lane = one chain: gamma(t) = ones at k_1 = G(v_0), k_{j+1} = k_j + 1 +
-// G(v_j) while k < n, G(v) = #{g < n : Cg[g] <= v} (an upper-bound binary
-// search of the image's table at `geo`), skip words v(chain, t, m) =
+// G(v_j) while k < n, G(v) = #{g < n : Cg[g] <= v} (geometric_skip over the
+// image's table at `geo`), skip words v(chain, t, m) =
 // Philox((2^31 + m/4, chain, t)).  Each flip ORs this lane's bit into the
 // gamma word of its node (gam = buffer base, word i at gam + 4 i).  Returns
 // the ballot of lanes with gamma(t) != 0.  The first word decides "any
 // flip" with one compare (G(v_0) < n iff v_0 < Cg[n-1]).
 template <bool SMEM>
-__device__ __forceinline__ uint32_t geometric_gamma(const Img<SMEM>& img, uint32_t geo, int n, uint32_t chain,
-                                                    uint32_t t_lo, uint32_t t_hi, const uint32_t* __restrict__ rk,
-                                                    uint32_t gam, uint32_t lmask, bool valid)
+__device__ __forceinline__ uint32_t geometric_gamma(const Img<SMEM>& img, uint32_t geo, int n, float inv_lnq,
+                                                    uint32_t chain, uint32_t t_lo, uint32_t t_hi,
+                                                    const uint32_t* __restrict__ rk, uint32_t gam, uint32_t lmask,
+                                                    bool valid)
 {
     uint32_t has = 0;
     if (valid) {
@@ -370,19 +371,29 @@ __device__ __forceinline__ uint32_t geometric_gamma(const Img<SMEM>& img, uint32
             for (uint32_t m = 0;; ++m) {
                 if (m > 0 && (m & 3u) == 0) v = philox4x32_10(0x80000000u + (m >> 2), chain, t_lo, t_hi, rk);
                 const uint32_t w = (m & 3u) == 0 ? v.x : (m & 3u) == 1 ? v.y : (m & 3u) == 2 ? v.z : v.w;
-                int lo = 0, hi = n;  // G = number of table entries <= w
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (img.ld32(geo + 4u * (uint32_t)mid) <= w) lo = mid + 1;
-                    else hi = mid;
-                }
-                k += 1 + lo;
+                k += 1 + geometric_skip(w, n, inv_lnq, [&](int g) { return img.ld32(geo + 4u * (uint32_t)g); });
                 if (k >= n) break;
                 asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(gam + 4u * (uint32_t)k), "r"(lmask) : "memory");
             }
         }
     }
     return __ballot_sync(FULL, has != 0u);
+}
+
+// G(w) = #{g < n : Cg[g] <= w} (Cg non-decreasing): an estimate from the
+// geometric law, g0 ~ ln(1 - w 2^-32) / ln(1 - p) (inv_lnq = 1 / ln(1 - p)),
+// corrected against the table until exact -- the result depends on the table
+// only, the estimate only sets where the (usually 0-2 step) search starts
+template <typename Load>
+__device__ __forceinline__ int geometric_skip(uint32_t w, int n, float inv_lnq, Load cg)
+{
+    const float x = (float)w * 2.3283064365386963e-10f;  // w 2^-32
+    float e = log1pf(-x) * inv_lnq;
+    e = fminf(fmaxf(e, 0.0f), (float)n);
+    int g = (int)e;
+    while (g < n && cg(g) <= w) ++g;
+    while (g > 0 && cg(g - 1) > w) --g;
+    return g;
 }
 
 // node records {E1, E2, E3, w} of one quad

@@ -166,9 +166,16 @@ __device__ __noinline__ uint32_t slow_bit_packed(uint32_t w, uint32_t u, uint32_
     return (tw >> (idx & 31u)) & 1u;
 }
 
-template <bool PER_NODE, int FT, bool SLOW>
+// MODE: 0 VECTOR, 1 PER_NODE, 2 VECTOR with the geometric-skip stream
+// (reading Q18): one warp per chain draws gamma(t) at the start of the step
+// (any flip <=> the first skip word is below Cg[n-1]; the flip positions by
+// skips over the image's table in global memory) into flip words Gm; a chain
+// with gamma != 0 takes s XOR gamma, so its node evaluation is skipped.
+template <int MODE, int FT, bool SLOW>
 __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_constant__ NodeParParams C)
 {
+    constexpr bool PER_NODE = MODE == 1;
+    constexpr bool GEO = MODE == 2;
     const TrajParams& P = C.T;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar_img;
@@ -191,10 +198,16 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
     const int NWp = (NW + 3) & ~3;
 
     // dynamic shared memory: S[2][G][NWp] packed state per step parity and
-    // chain, X[2][G][NWp] {f, gamma} exchange words, then the sub-image
+    // chain, X[2][G][NWp] {f, gamma} exchange words, Gm[2][G][NWp] geometric
+    // flip words and Gf[2][G4] flags per step parity, then the sub-image
+    const int G4 = (C.G + 3) & ~3;
     const uint32_t Sb = smem_u32(smem);
     const uint32_t Xb = Sb + 8u * (uint32_t)(C.G * NWp);
-    const uint32_t ibase = Xb + 16u * (uint32_t)(C.G * NWp);
+    const uint32_t Gmb = Xb + 16u * (uint32_t)(C.G * NWp);
+    const uint32_t Gfb = Gmb + 8u * (uint32_t)(C.G * NWp);
+    const uint32_t ibase = Gfb + 8u * (uint32_t)G4;
+    auto Gmp = [&](uint32_t par, int g) { return Gmb + 4u * (uint32_t)((2 * g + (int)par) * NWp); };
+    auto Gfp = [&](uint32_t par, int g) { return Gfb + 4u * (uint32_t)((int)par * G4 + g); };
     auto Sp = [&](uint32_t par, int g) { return Sb + 4u * (uint32_t)((2 * g + (int)par) * NWp); };
     auto Xp = [&](uint32_t par, int g) { return Xb + 8u * (uint32_t)((2 * g + (int)par) * NWp); };
 
@@ -252,6 +265,44 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
         }
         if (lane == 0) sts32(Sp(0, g) + 4u * (uint32_t)j, v);
     }
+    // A4 of the geometric stream (reading Q18) for chain g at step t into the
+    // parity `par` buffers: gamma(t) != 0 iff the first skip word is below
+    // Cg[n-1]; then the flip positions by skips over the table (global
+    // memory, L1-cached).  Every CTA draws the whole gamma(t) of its chains
+    // (the commit applies it locally), one step AHEAD, so that a chain-step
+    // with gamma != 0 skips its node evaluation and the draw is off the
+    // step's critical path.
+    auto geo_draw = [&](int g, uint64_t tt, uint32_t par) {
+        const uint32_t Gm = Gmp(par, g), Gf = Gfp(par, g);
+        if (lds32(Gf))  // the flips of two steps ago: clear their words
+            for (int j = lane; j < NW; j += 32) sts32(Gm + 4u * (uint32_t)j, 0u);
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t chain = (uint32_t)(P.chain_base + chain0 + g);
+            uint32_t any = 0;
+            uint4 v = philox4x32_10(0x80000000u, chain, (uint32_t)tt, (uint32_t)(tt >> 32), P.rk);
+            if (v.x < C.geo_last) {
+                any = 1;
+                int k = -1;
+                for (uint32_t m = 0;; ++m) {
+                    if (m > 0 && (m & 3u) == 0)
+                        v = philox4x32_10(0x80000000u + (m >> 2), chain, (uint32_t)tt, (uint32_t)(tt >> 32), P.rk);
+                    const uint32_t w = (m & 3u) == 0 ? v.x : (m & 3u) == 1 ? v.y : (m & 3u) == 2 ? v.z : v.w;
+                    k += 1 + geometric_skip(w, n, P.geo_inv_lnq, [&](int gg) { return __ldg(C.geo_table + gg); });
+                    if (k >= n) break;
+                    const uint32_t a = Gm + 4u * (uint32_t)(k >> 5);
+                    sts32(a, lds32(a) | (1u << (k & 31)));
+                }
+            }
+            sts32(Gf, any);
+        }
+        __syncwarp();
+    };
+    if (GEO) {
+        for (int i = tid; i < 2 * C.G * NWp + 2 * G4; i += T) sts32(Gmb + 4u * i, 0u);  // flips start zero
+        __syncthreads();
+        for (int g = wg; g < Ge; g += NWARP) geo_draw(g, (uint64_t)(P.step0 + 1), 1u);  // step 1's gamma
+    }
     __syncthreads();
     // every CTA is staged and its barriers armed before any peer stores
     np_cluster_sync();
@@ -270,6 +321,10 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
         const uint32_t par = (uint32_t)(r & 1);
         const uint32_t bar = par ? bx1 : bx0;
         const uint64_t t = (uint64_t)(P.step0 + r);
+        // the geometric stream's gamma(t+1): drawn first by the last warps, so
+        // that its latency overlaps this step's node work and exchange
+        if (GEO && r < total)
+            for (int g = NWARP - 1 - wg; g >= 0 && g < Ge; g += NWARP) geo_draw(g, t + 1, par ^ 1u);
         // ---- A3-A6: warp = (chain g, own word j), lane = node 32 j + lane ----
         // (items it = g OW + (j - w_lo) strided by the warp count, walked
         // without integer division)
@@ -281,6 +336,15 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
             }
             const int j = w_lo + jj;
             const uint32_t chain = (uint32_t)(P.chain_base + chain0 + g);
+            const uint32_t a = Xp(par, g) + 8u * (uint32_t)j;
+            if (GEO && lds32(Gfp(par, g))) {
+                // gamma(t) != 0: s_t = s_{t-1} XOR gamma, applied by
+                // every CTA from its own draw at the commit; nothing to evaluate
+                if (lane == 0) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(0u), "r"(0u) : "memory");
+                if (lane < (int)K && lane != (int)rank)
+                    st_async_v2(np_map_peer(a, (uint32_t)lane), 0u, 0u, np_map_peer(bar, (uint32_t)lane));
+                continue;
+            }
             const uint32_t So = Sp(par ^ 1u, g);
             const uint32_t i = 32u * (uint32_t)j + (uint32_t)lane;
             const bool live = (int)i < n;
@@ -306,7 +370,6 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
             // A7: the word of 32 nodes, f and gamma
             const uint32_t vf = __ballot_sync(FULL, live && bit);
             const uint32_t vg = __ballot_sync(FULL, live && gm);
-            const uint32_t a = Xp(par, g) + 8u * (uint32_t)j;
             // lane 0 keeps it, lane p < K pushes it to peer p (one instruction for all peers)
             if (lane == 0) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(vf), "r"(vg) : "memory");
             if (lane < (int)K && lane != (int)rank)
@@ -321,12 +384,15 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
         for (int g = wg; g < Ge; g += NWARP) {
             const uint32_t So = Sp(par ^ 1u, g), Sn = Sp(par, g), X = Xp(par, g);
             uint32_t anyg = 0;
-            if (!PER_NODE)
+            if (!PER_NODE && !GEO)
                 for (int j = lane; j < NW; j += 32) anyg |= lds32(X + 8u * (uint32_t)j + 4u);
-            const bool any = PER_NODE ? false : __any_sync(FULL, anyg != 0u);
+            const bool any = PER_NODE ? false : GEO ? lds32(Gfp(par, g)) != 0u : __any_sync(FULL, anyg != 0u);
+            // gamma words: exchanged (VECTOR) or this CTA's own draw (GEO)
+            const uint32_t Gw = GEO ? Gmp(par, g) : X + 4u;
+            const uint32_t Gs = GEO ? 4u : 8u;
             for (int j = lane; j < NW; j += 32) {
                 uint32_t v = lds32(X + 8u * (uint32_t)j);
-                if (!PER_NODE && any) v = lds32(So + 4u * (uint32_t)j) ^ lds32(X + 8u * (uint32_t)j + 4u);
+                if (!PER_NODE && any) v = lds32(So + 4u * (uint32_t)j) ^ lds32(Gw + Gs * (uint32_t)j);
                 sts32(Sn + 4u * (uint32_t)j, v);
             }
         }
@@ -357,29 +423,30 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
     np_cluster_sync();
 }
 
-template <bool PER_NODE, int FT, bool SLOW>
+template <int MODE, int FT, bool SLOW>
 const void* nkptr()
 {
-    return reinterpret_cast<const void*>(&traj_nodepar_kernel<PER_NODE, FT, SLOW>);
+    return reinterpret_cast<const void*>(&traj_nodepar_kernel<MODE, FT, SLOW>);
 }
 
-template <bool PER_NODE>
+template <int MODE>
 const void* npick_ft(int FT, bool slow)
 {
     switch (FT) {
-        case 3: return slow ? nkptr<PER_NODE, 3, true>() : nkptr<PER_NODE, 3, false>();
-        case 4: return slow ? nkptr<PER_NODE, 4, true>() : nkptr<PER_NODE, 4, false>();
-        case 5: return slow ? nkptr<PER_NODE, 5, true>() : nkptr<PER_NODE, 5, false>();
-        case 6: return slow ? nkptr<PER_NODE, 6, true>() : nkptr<PER_NODE, 6, false>();
-        case 7: return slow ? nkptr<PER_NODE, 7, true>() : nkptr<PER_NODE, 7, false>();
-        default: return slow ? nkptr<PER_NODE, 8, true>() : nkptr<PER_NODE, 8, false>();
+        case 3: return slow ? nkptr<MODE, 3, true>() : nkptr<MODE, 3, false>();
+        case 4: return slow ? nkptr<MODE, 4, true>() : nkptr<MODE, 4, false>();
+        case 5: return slow ? nkptr<MODE, 5, true>() : nkptr<MODE, 5, false>();
+        case 6: return slow ? nkptr<MODE, 6, true>() : nkptr<MODE, 6, false>();
+        case 7: return slow ? nkptr<MODE, 7, true>() : nkptr<MODE, 7, false>();
+        default: return slow ? nkptr<MODE, 8, true>() : nkptr<MODE, 8, false>();
     }
 }
 
 const void* npick(const NodeParParams& C)
 {
-    return C.T.per_node ? npick_ft<true>(C.T.L.fast_theta, C.T.L.slow_nodes > 0)
-                        : npick_ft<false>(C.T.L.fast_theta, C.T.L.slow_nodes > 0);
+    const int FT = C.T.L.fast_theta;
+    const bool slow = C.T.L.slow_nodes > 0;
+    return C.T.per_node ? npick_ft<1>(FT, slow) : C.T.geometric ? npick_ft<2>(FT, slow) : npick_ft<0>(FT, slow);
 }
 
 cudaLaunchConfig_t ncfg(const NodeParParams& C, int threads, size_t smem, unsigned grid, cudaLaunchAttribute* attr)
@@ -409,7 +476,7 @@ cudaError_t nprepare(const void* fn, const NodeParParams& C, size_t smem)
 size_t nodepar_smem_bytes(int n_words, int G, uint32_t max_sub_image)
 {
     const size_t NWp = ((size_t)n_words + 3) & ~(size_t)3;
-    return (8u + 16u) * NWp * (size_t)G + max_sub_image;
+    return (8u + 16u + 8u) * NWp * (size_t)G + 8u * (((size_t)G + 3) & ~(size_t)3) + max_sub_image;
 }
 
 int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, void* stream)

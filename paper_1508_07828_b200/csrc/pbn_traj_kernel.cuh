@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
         // gamma(t) and marks it in the gamma words; the VECTOR fix-up after
         // the step barrier applies it (the node words carry no perturbation)
         if (GEO && wg == 0)
-            any |= geometric_gamma(img, (SMEM ? sbase : 0u) + P.L.geo_off, n, chain, t_lo, t_hi, P.rk, gam, lmask,
-                                   valid);
+            any |= geometric_gamma(img, (SMEM ? sbase : 0u) + P.L.geo_off, n, P.geo_inv_lnq, chain, t_lo, t_hi, P.rk,
+                                   gam, lmask, valid);
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
         // them (and their gamma words if any)

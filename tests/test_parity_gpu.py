@@ -566,11 +566,30 @@ def test_geometric_mode_C4_sampled_chains_and_launch_shapes(pbn):
         assert np.array_equal(ref[k], b[k]), ("global image", k)
 
 
-def test_geometric_mode_rejects_other_kernels(pbn):
+def test_geometric_mode_rejects_the_cluster_kernel(pbn):
     import paper_1508_07828_b200 as P
     model, pred = config_model("C2"), config_predicate("C2")
     pm = pbn.pbn_load(model, geometric=True)
     with pytest.raises(P.PbnError):
         gpu_run(pm, model, pred, n_chains=40, steps=10, cluster_size=2)
-    with pytest.raises(P.PbnError):
-        gpu_run(pm, model, pred, n_chains=40, steps=10, layout=NODE_LANES)
+
+
+@pytest.mark.parametrize("key,K,G", [("C1", 1, 1), ("C2", 2, 3), ("C3", 4, 2), ("C5", 8, 2)])
+def test_geometric_mode_node_lanes(pbn, key, K, G):
+    """Lanes over nodes with the geometric stream (chain-steps with gamma != 0
+    skip the evaluation): identical to K1 and to the oracle."""
+    c = CONFIGS[key]
+    model, pred = config_model(key), config_predicate(key)
+    pm = pbn.pbn_load(model, geometric=True)
+    chains = 5
+    steps, burn_in = min(c.steps, 2000), min(c.burn_in, 300)
+    kw = dict(n_chains=chains, steps=steps, burn_in=burn_in, seed=c.sim_seed, batch=c.batch)
+    a = gpu_run(pm, model, pred, cluster_size=1, layout=1, **kw)
+    b = gpu_run(pm, model, pred, cluster_size=K, layout=NODE_LANES, chains_per_cluster=G, **kw)
+    for k in ALL:
+        assert np.array_equal(a[k], b[k]), k
+    st, I, ws = oracle_run(model, pred, np.arange(chains), steps=steps, burn_in=burn_in, seed=c.sim_seed,
+                           batch=c.batch, geometric=True, threads=os.cpu_count() or 8)
+    packed = pack_states(st)
+    for j in range(chains):
+        compare_chain(b, j, packed[j], ws[j], steps, c.batch)
