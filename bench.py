@@ -306,6 +306,46 @@ def run_sweep(args, cfg, model, pred):
 
 
 # --------------------------------------------------------------------------
+def run_protocol(args):
+    """The whole method on the GPU through pbn_run (Algorithm 3, then 4 or 5,
+    the paper's unit of work, Table 1): C2 with the two-state rule
+    (BASELINE config 2), C3 with Skart (config 3).  Reports the decisions, the
+    pooled sample, the transitions simulated and the device time; not the
+    driver's bench line."""
+    import torch
+    import paper_1508_07828_b200 as pbn
+    torch.cuda.set_device(0)
+    for key in args.protocol.split(","):
+        cfg = CONFIGS[key]
+        model, pred = config_model(key), config_predicate(key)
+        pm = pbn.pbn_load(model)
+        x = cfg.extra
+        if key == "C3":
+            kw = dict(method=1, omega=cfg.chains, psi0=cfg.burn_in, rhat_threshold=1.1, h_star=x["h_star"],
+                      alpha_conf=x["alpha_conf"], seed=cfg.sim_seed, pred=pred, max_steps=1 << 22)
+        else:
+            kw = dict(method=0, omega=cfg.chains, psi0=x.get("psi0", 1000), rhat_threshold=x.get("rhat_threshold", 1.1),
+                      r=x.get("r", 0.01), s=x.get("s", 0.95), eps=x.get("eps", 1e-10), seed=cfg.sim_seed, pred=pred,
+                      max_steps=1 << 24)
+        pbn.pbn_run(pm, **kw)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st, res, err = pbn.pbn_run(pm, **kw)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        nu = cfg.chains * res.steps_per_chain * model.n
+        print(json.dumps({"protocol": key, "method": "skart" if kw["method"] == 1 else "two-state", "status": st,
+                          "err": err, "omega": cfg.chains, "psi": res.psi, "gr_iterations": res.gr_iterations,
+                          "rhat": res.rhat, "extensions": res.extensions, "M": res.M, "N": res.N,
+                          "sample_size": res.sample_size, "steps_per_chain": res.steps_per_chain,
+                          "estimate": res.estimate, "ci": [res.ci_lo, res.ci_hi], "seconds": dt,
+                          "node_updates_per_s": nu / dt,
+                          "note": "wall time of pbn_run (GPU kernels + host statistics + D2H decision reads)"}),
+              flush=True)
+        pm.close()
+
+
+# --------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -324,6 +364,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
     ap.add_argument("--sweep", action="store_true", help="C5 chain-count sweep (one line per count)")
     ap.add_argument("--e2e-steps", type=int, default=3, help="timed end-to-end (host buffer) iterations")
+    ap.add_argument("--protocol", default="",
+                    help="time the whole method (pbn_run) on C2 and/or C3, e.g. --protocol C2,C3")
     ap.add_argument("--geometric", action="store_true",
                     help="geometric-skip perturbation stream (NEXT-2, PBN_PERTURB_GEOMETRIC)")
     args = ap.parse_args()
@@ -344,6 +386,9 @@ def main():
 
     if args.sweep:
         run_sweep(args, cfg, model, pred)
+        return
+    if args.protocol:
+        run_protocol(args)
         return
     if args.impl == "reference":
         run_reference(args, cfg, model, pred, rank)
