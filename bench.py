@@ -334,7 +334,16 @@ def run_protocol(args):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         nu = cfg.chains * res.steps_per_chain * model.n
-        print(json.dumps({"protocol": key, "method": "skart" if kw["method"] == 1 else "two-state", "status": st,
+        cpu = None
+        if key == "C2" and not args.no_cpu_baseline:
+            # cpu_baseline leg: the oracle's Algorithm 3 + 4 on the same inputs
+            from oracle import driver as odr
+            t1 = time.perf_counter()
+            o = odr.parallel_two_state(model, pred, cfg.sim_seed, cfg.chains, kw["psi0"], kw["rhat_threshold"],
+                                       kw["r"], kw["s"], kw["eps"], kw["max_steps"], threads=ncores())
+            cpu = {"seconds": time.perf_counter() - t1, "cores": ncores(), "kind": "oracle",
+                   "same_decisions": (o.psi, o.sample_size, o.M, o.N) == (res.psi, res.sample_size, res.M, res.N)}
+        print(json.dumps({"protocol": key, "cpu_baseline": cpu, "method": "skart" if kw["method"] == 1 else "two-state", "status": st,
                           "err": err, "omega": cfg.chains, "psi": res.psi, "gr_iterations": res.gr_iterations,
                           "rhat": res.rhat, "extensions": res.extensions, "M": res.M, "N": res.N,
                           "sample_size": res.sample_size, "steps_per_chain": res.steps_per_chain,
