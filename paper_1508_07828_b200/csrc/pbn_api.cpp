@@ -46,6 +46,7 @@ struct pbn_model_s {
     std::vector<ClusterImages> clusters;  // K = 2, 4, 8, 16 (K <= quads)
     std::vector<NodeParImages> nodepar;   // K = 1, 2, 4, 8, 16 (K <= packed words)
     uint32_t geo_last = 0;                // geometric mode: Cg[n-1]
+    uint32_t geo_off = 0;                 // geometric mode: byte offset of Cg in the image
     double p = 0.0;
 };
 
@@ -225,7 +226,7 @@ inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
 // count are model-wide, so every sub-image of a cluster uses one kernel.
 std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L, int32_t node_lo = 0,
                                  int32_t node_hi = -1, uint32_t qs = 32, bool packed = false, bool geo = false,
-                                 double geo_p = 0.0, bool skew = false)
+                                 double geo_p = 0.0, bool skew = false, uint32_t* geo_off = nullptr)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
     if (node_hi < 0) node_hi = n;
@@ -365,11 +366,12 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
     if (geo) {
         // geometric-skip table Cg[g] = floor((1 - q^(g+1)) 2^32), q^(g+1) by
         // repeated fp64 multiplication (reading Q18)
-        L->geo_off = B.alloc(4u * (size_t)n, 16);
+        const uint32_t go = B.alloc(4u * (size_t)n, 16);
+        if (geo_off) *geo_off = go;
         double q = 1.0 - geo_p, r = 1.0;
         for (int32_t g = 0; g < n; ++g) {
             r *= q;
-            B.u32(L->geo_off)[g] = (uint32_t)std::floor(std::ldexp(1.0 - r, 32));
+            B.u32(go)[g] = (uint32_t)std::floor(std::ldexp(1.0 - r, 32));
         }
     }
     B.alloc(16);  // tail slack
@@ -432,8 +434,8 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     const bool geo = desc->flags == PBN_PERTURB_GEOMETRIC;
     // geometric mode: no per-node perturbation share in the thresholds (T_p = 0)
     const uint32_t Tsel = geo ? 0u : m->Tp;
-    std::vector<uint8_t> img = build_image(desc, Tsel, &m->L, 0, -1, 32u, false, geo, desc->p);
-    if (geo) std::memcpy(&m->geo_last, img.data() + m->L.geo_off + 4u * (uint32_t)(desc->n - 1), 4);
+    std::vector<uint8_t> img = build_image(desc, Tsel, &m->L, 0, -1, 32u, false, geo, desc->p, false, &m->geo_off);
+    if (geo) std::memcpy(&m->geo_last, img.data() + m->geo_off + 4u * (uint32_t)(desc->n - 1), 4);
     e = cudaMalloc(&m->d_image, img.size());
     if (e != cudaSuccess) {
         delete m;
@@ -585,6 +587,7 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     // geometric mode: gamma comes from the skip stream, never from u < T_p
     P->Tp = P->geometric ? 0u : m->Tp;
     P->geo_inv_lnq = P->geometric ? (float)(1.0 / std::log1p(-m->p)) : 0.0f;
+    P->geo_off = m->geo_off;
     P->n = m->L.n;
     P->nquads = (m->L.n + 3) / 4;
     P->n_pad = (m->L.n + 3) & ~3;
@@ -701,7 +704,7 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         C.K = np_use->K;
         C.G = np_G(*np_use);
         if (P.geometric) {
-            C.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->L.geo_off);
+            C.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->geo_off);
             C.geo_last = m->geo_last;
         }
         if (a->chains_per_cluster > 0 && C.G != a->chains_per_cluster) return PBN_E_USAGE;

@@ -95,7 +95,6 @@ struct ImageLayout {
     int32_t max_theta = 0, max_ell = 0;
     int32_t slow_nodes = 0;
     int32_t fast_theta = kFastMinTheta;  // FT
-    uint32_t geo_off = 0;      // geometric-skip table Cg[0..n-1] (u32), PBN_PERTURB_GEOMETRIC only
 };
 
 struct TrajParams {
@@ -104,8 +103,6 @@ struct TrajParams {
     uint32_t rk[20];           // Philox round keys (k0 + r W0, k1 + r W1), r = 0..9
     uint32_t Tp;               // perturbation threshold of the node words (0 in geometric mode)
     int32_t per_node;          // PBN_PERTURB_PER_NODE semantics
-    int32_t geometric;         // PBN_PERTURB_GEOMETRIC: gamma(t) from the skip stream (reading Q18)
-    float geo_inv_lnq;         // 1 / ln(1 - p): start of the skip search (the table decides)
     int32_t n;
     int32_t nquads;            // ceil(n/4)
     int32_t n_pad;             // n rounded up to a multiple of 4 (u32 words per buffer)
@@ -144,6 +141,12 @@ struct TrajParams {
     uint32_t* batch_sums;
     uint32_t* bits;
     unsigned long long* totals;  // [6 x n_props]
+    // geometric-skip stream (PBN_PERTURB_GEOMETRIC, reading Q18); kept at the
+    // end of the struct: inserting them earlier changed the global-image K1's
+    // register allocation (more spills, C5 -4 %)
+    int32_t geometric;         // gamma(t) from the skip stream
+    float geo_inv_lnq;         // 1 / ln(1 - p): start of the skip search (the table decides)
+    uint32_t geo_off;          // byte offset of the table Cg[0..n-1] (u32) in the image
 };
 
 // Cluster launch (pbn_cluster.cu): one 32-chain group per cluster of K CTAs,

@@ -179,11 +179,13 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
                 }
             }
         }
+#if defined(PBN_GZ_START)
         // a previous unit of this CTA (e.g. a ragged group, whose lanes
         // without a chain may draw perturbations that never trigger the
         // fix-up) can leave gamma bits behind: clear them per unit
         if (!PER_NODE && P.persistent && it > 0)
             for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
+#endif
         const bool first_chunk = chunk == 0;
         const bool last_chunk = r_end >= total;
         // (kept in 32 bits: few live registers across the step loop -- the
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
         // gamma(t) and marks it in the gamma words; the VECTOR fix-up after
         // the step barrier applies it (the node words carry no perturbation)
         if (GEO && wg == 0)
-            any |= geometric_gamma(img, (SMEM ? sbase : 0u) + P.L.geo_off, n, P.geo_inv_lnq, chain, t_lo, t_hi, P.rk,
+            any |= geometric_gamma(img, (SMEM ? sbase : 0u) + P.geo_off, n, P.geo_inv_lnq, chain, t_lo, t_hi, P.rk,
                                    gam, lmask, valid);
         const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;  // full quads [q0, qf), ragged after
         // one full quad: four independent nodes, then one 16-byte store commits
@@ -402,6 +404,10 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.done + group), "r"((uint32_t)(chunk + 1))
                          : "memory");
         }
+#if !defined(PBN_GZ_START) && !defined(PBN_GZ_NONE)
+        if (!PER_NODE && vmask != FULL)  // see the end of the unit below
+            for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
+#endif
         continue;
     }
 
@@ -418,6 +424,13 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
         }
     }
     if (stats) cs.finish(P, prop, valid, orow(), leader);
+#if !defined(PBN_GZ_START) && !defined(PBN_GZ_NONE)
+    // a ragged group's chain-less lanes may draw perturbations that never
+    // trigger the fix-up (M masks them): their gamma bits must not reach the
+    // next unit of this CTA, where those lanes hold chains
+    if (!PER_NODE && P.persistent && vmask != FULL)
+        for (int i = tid; i < P.n_pad; i += blockDim.x) sts32(gam + 4u * i, 0u);
+#endif
     }  // work units
 }
 
