@@ -15,6 +15,64 @@
 #include "../../include/pbnsim.h"
 #include "pbn_internal.h"
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
+namespace pbn {
+
+namespace {
+std::mutex g_cache_mu;
+std::map<const void*, std::pair<size_t, bool>> g_func_smem;
+std::map<std::tuple<const void*, int, size_t>, int> g_occ;
+std::map<std::pair<int, int>, int> g_dev_attr;
+}  // namespace
+
+cudaError_t ensure_func_smem(const void* fn, size_t bytes, bool nonportable_cluster)
+{
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto& e = g_func_smem[fn];
+    if (bytes > e.first) {
+        const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (r != cudaSuccess) return r;
+        e.first = bytes;
+    }
+    if (nonportable_cluster && !e.second) {
+        const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (r != cudaSuccess) return r;
+        e.second = true;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t cached_blocks_per_sm(const void* fn, int threads, size_t smem, int* out)
+{
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    const auto key = std::make_tuple(fn, threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    const cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, threads, smem);
+    if (r == cudaSuccess) g_occ[key] = *out;
+    return r;
+}
+
+int cached_device_attr(cudaDeviceAttr attr, int device)
+{
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    const auto key = std::make_pair((int)attr, device);
+    auto it = g_dev_attr.find(key);
+    if (it != g_dev_attr.end()) return it->second;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, attr, device) != cudaSuccess) return 0;
+    g_dev_attr[key] = v;
+    return v;
+}
+
+}  // namespace pbn
+
 // Sub-images of one cluster size K (pbn_cluster.cu), concatenated on the device.
 struct ClusterImages {
     int K = 0;
@@ -645,10 +703,9 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     if (a->n_chains == 0) return PBN_OK;
     if (a->cluster_size < 0 || a->cluster_size > pbn::kMaxCluster) return PBN_E_USAGE;
     // ---- one CTA per group (K1) or a cluster of K CTAs per group (K1c) ----
-    int smem_optin = 0, sms = 0;
-    if (cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device) != cudaSuccess)
-        return PBN_E_CUDA;
+    const int smem_optin = pbn::cached_device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device);
+    const int sms = pbn::cached_device_attr(cudaDevAttrMultiProcessorCount, m->device);
+    if (smem_optin <= 0 || sms <= 0) return PBN_E_CUDA;
     const size_t limit = (size_t)smem_optin - 64;
     const int64_t groups = (a->n_chains + 31) / 32;
     if (a->layout < PBN_LAYOUT_AUTO || a->layout > PBN_LAYOUT_NODE_LANES) return PBN_E_USAGE;

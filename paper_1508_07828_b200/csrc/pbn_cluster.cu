@@ -323,12 +323,8 @@ int launch_traj_cluster(const ClusterParams& C, int warps, size_t smem_bytes, vo
 {
     const void* fn = C.T.per_node ? cpick_ft<true>(C.T.L.fast_theta, C.T.L.slow_nodes > 0)
                                   : cpick_ft<false>(C.T.L.fast_theta, C.T.L.slow_nodes > 0);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    cudaError_t e = ensure_func_smem(fn, smem_bytes, C.K > 8);
     if (e != cudaSuccess) return (int)e;
-    if (C.K > 8) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return (int)e;
-    }
     const int64_t groups = (C.T.n_chains + 31) / 32;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(groups * C.K));
@@ -351,12 +347,8 @@ int max_active_clusters(const ClusterParams& C, int warps, size_t smem_bytes, in
 {
     const void* fn = C.T.per_node ? cpick_ft<true>(C.T.L.fast_theta, C.T.L.slow_nodes > 0)
                                   : cpick_ft<false>(C.T.L.fast_theta, C.T.L.slow_nodes > 0);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    cudaError_t e = ensure_func_smem(fn, smem_bytes, C.K > 8);
     if (e != cudaSuccess) return (int)e;
-    if (C.K > 8) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return (int)e;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)C.K);
     cfg.blockDim = dim3((unsigned)(warps * 32));

@@ -195,6 +195,14 @@ struct LaunchPlan {
     bool image_in_smem;
 };
 
+// Host-side launch caches (pbn_api.cpp; thread-safe): the per-kernel
+// dynamic shared-memory limit is raised once (never lowered), occupancy
+// answers and device attributes are computed once per key -- pbn_simulate
+// repeats none of these driver calls on its hot path.
+cudaError_t ensure_func_smem(const void* fn, size_t bytes, bool nonportable_cluster);
+cudaError_t cached_blocks_per_sm(const void* fn, int threads, size_t smem, int* out);
+int cached_device_attr(cudaDeviceAttr attr, int device);
+
 // Implemented in pbn_traj.cu.  Returns 0 on success, a cudaError_t value on a
 // CUDA failure, or -1 (with *why set) when the sizes cannot be served.
 int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why);

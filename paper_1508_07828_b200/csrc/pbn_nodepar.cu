@@ -466,9 +466,7 @@ cudaLaunchConfig_t ncfg(const NodeParParams& C, int threads, size_t smem, unsign
 
 cudaError_t nprepare(const void* fn, const NodeParParams& C, size_t smem)
 {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess && C.K > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    return e;
+    return ensure_func_smem(fn, smem, C.K > 8);
 }
 
 }  // namespace

@@ -64,9 +64,7 @@ constexpr int kGlobalImageThreads = PBN_GLOBAL_THREADS < PBN_MAX_THREADS ? PBN_G
 
 int sm_count(int device)
 {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
-    return v;
+    return cached_device_attr(cudaDevAttrMultiProcessorCount, device);
 }
 
 const void* pick_kernel(bool smem, int mode, int FT, bool slow)
@@ -100,9 +98,8 @@ int default_warps(int nquads)
 
 int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why)
 {
-    int smem_optin = 0;
-    cudaError_t e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    if (e != cudaSuccess) return (int)e;
+    const int smem_optin = cached_device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (smem_optin <= 0) return (int)cudaErrorInvalidDevice;
     const size_t static_smem = 64;  // mbarrier + slack
     const size_t limit = (size_t)smem_optin - static_smem;
     const size_t group_bytes = (size_t)P.group_words * 4;
@@ -155,7 +152,7 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
     P.image_smem_bytes = plan.image_in_smem ? P.L.bytes : 0u;
     const int mode = P.per_node ? 1 : P.geometric ? 2 : 0;
     const void* fn = pick_kernel(plan.image_in_smem, mode, P.L.fast_theta, P.L.slow_nodes > 0);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
+    cudaError_t e = ensure_func_smem(fn, plan.smem_bytes, false);
     if (e != cudaSuccess) return (int)e;
     cudaStream_t s = (cudaStream_t)stream;
 
@@ -164,7 +161,7 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
     const int64_t G = (P.n_chains + 31) / 32;
     const int64_t total = P.burn_in + P.steps;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, plan.threads, plan.smem_bytes);
+    e = cached_blocks_per_sm(fn, plan.threads, plan.smem_bytes, &per_sm);
     if (e != cudaSuccess) return (int)e;
     const int64_t resident = (int64_t)sm_count(device) * std::max(per_sm, 1);
     bool persistent = false;
