@@ -284,7 +284,7 @@ inline uint32_t table_bit(const pbn_model_desc* d, int32_t f, uint32_t idx)
 // count are model-wide, so every sub-image of a cluster uses one kernel.
 std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::ImageLayout* L, int32_t node_lo = 0,
                                  int32_t node_hi = -1, uint32_t qs = 32, bool packed = false, bool geo = false,
-                                 double geo_p = 0.0, bool skew = false, uint32_t* geo_off = nullptr)
+                                 double geo_p = 0.0, uint32_t* geo_off = nullptr)
 {
     const int32_t n = d->n, nf = d->fn_off[n];
     if (node_hi < 0) node_hi = n;
@@ -323,17 +323,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
         uint32_t w3 = 0;  // nrec[i].w, written last (B.alloc may move the buffer)
         if (fast[i]) {
             const int32_t tm = FT;  // every fast function is padded to the model-wide FT
-            const uint32_t ds = pbn::desc_bytes(tm);
-            if (packed && skew) {
-                // lanes over nodes: the 32 lanes of a warp read the selected
-                // descriptors of 32 consecutive nodes; skew each node's block
-                // to start at 16 (i mod 8) modulo 128 bytes so those 16-byte
-                // chunks spread over all 32 banks (C5 K1n: an LDS.128 of
-                // descriptors cost 19.8 wavefronts with 64-byte-aligned blocks)
-                // -- at up to 112 padding bytes per node
-                const size_t want = 16u * (size_t)(i & 7);
-                while ((B.buf.size() & 127u) != want) B.alloc(16, 16);
-            }
+            const uint32_t ds = packed ? pbn::desc_bytes_packed(tm) : pbn::desc_bytes(tm);
             const uint32_t off_desc = B.alloc((size_t)ds * ell, 16);
             for (int32_t j = 0; j < ell; ++j) {
                 const int32_t f = f0 + j;
@@ -345,6 +335,25 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                     T[idx >> 5] |= table_bit(d, f, idx >> (tm - theta)) << (idx & 31u);
                 uint32_t* w = B.u32(off_desc + ds * (uint32_t)j);
                 const uint32_t wbase = off_desc + ds * (uint32_t)j;
+                if (packed) {
+                    // lanes over nodes: parents as u16 node ids (the K1n state is
+                    // bit-packed), so a descriptor is one 16-byte chunk (FT <= 5)
+                    // plus table words -- half the lane-divergent shared-memory
+                    // wavefronts of the u32 layout; pad parents read node 0
+                    auto pid = [&](int32_t m) -> uint32_t {
+                        return m < theta ? (uint32_t)d->parents[d->par_off[f] + m] : 0u;
+                    };
+                    const int32_t na = tm >= 7 ? 8 : tm;  // u16 parent slots
+                    const int32_t a0 = tm >= 7 ? 0 : (tm == 6 ? 2 : 1);  // first word of the u16 pairs
+                    for (int32_t m = 0; m < na; ++m) w[a0 + m / 2] |= pid(m) << (16 * (m & 1));
+                    if (tm >= 7) {
+                        for (size_t q = 0; q < T.size(); ++q) w[4 + q] = reverse_bits(T[q]);
+                    } else {
+                        w[0] = reverse_bits(T[0]);
+                        if (tm == 6) w[1] = reverse_bits(T[1]);
+                    }
+                    continue;
+                }
                 auto par = [&](int32_t m) {
                     const uint32_t node = m < theta ? d->parents[d->par_off[f] + m] : 0u;
                     return packed ? node : pbn::state_off(node, qs);
@@ -357,17 +366,6 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                     }
                     // stored bit-reversed per word: entry e at bit 31 - (e & 31)
                     for (size_t q = 0; q < T.size(); ++q) w[8 + q] = reverse_bits(T[q]);
-                    if (packed && tm == 8) {
-                        // lanes over nodes: XOR-swizzle the 4 16-byte chunks by the
-                        // descriptor's own 64-byte index (mod 4) so that the
-                        // selected descriptors of 32 consecutive nodes spread
-                        // over the banks (fast_bit_packed<8> undoes it)
-                        const uint32_t sw = (wbase >> 6) & 3u;
-                        uint32_t logical[16];
-                        for (int q = 0; q < 16; ++q) logical[q] = w[q];
-                        for (uint32_t c = 0; c < 4; ++c)
-                            for (uint32_t k = 0; k < 4; ++k) w[4u * (c ^ sw) + k] = logical[4u * c + k];
-                    }
                 } else {
                     int k = 0;
                     w[k++] = reverse_bits(T[0]);
@@ -492,7 +490,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     const bool geo = desc->flags == PBN_PERTURB_GEOMETRIC;
     // geometric mode: no per-node perturbation share in the thresholds (T_p = 0)
     const uint32_t Tsel = geo ? 0u : m->Tp;
-    std::vector<uint8_t> img = build_image(desc, Tsel, &m->L, 0, -1, 32u, false, geo, desc->p, false, &m->geo_off);
+    std::vector<uint8_t> img = build_image(desc, Tsel, &m->L, 0, -1, 32u, false, geo, desc->p, &m->geo_off);
     if (geo) std::memcpy(&m->geo_last, img.data() + m->geo_off + 4u * (uint32_t)(desc->n - 1), 4);
     e = cudaMalloc(&m->d_image, img.size());
     if (e != cudaSuccess) {
@@ -542,31 +540,15 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     // packed sub-images for the lanes-over-nodes kernel: CTA r of a K-cluster
     // owns packed state words [W r / K, W (r+1) / K)
     const int32_t nw = (desc->n + 31) / 32;
-    int smem_optin = 0;
-    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     for (int K = 1; K <= pbn::kMaxCluster && K <= nw; K *= 2) {
         NodeParImages ni;
         ni.K = K;
         std::vector<uint8_t> all;
         for (int r = 0; r <= K; ++r) ni.w_lo[r] = (int32_t)((int64_t)nw * r / K);
-        // skewed descriptor blocks when the padded sub-images still fit one
-        // CTA's shared memory, else the compact layout (C5: K = 4 fits only
-        // compact, and K = 4 is its fastest 64-chain cluster size)
-        bool skew = true;
-        {
-            uint32_t mx = 0;
-            for (int r = 0; r < K; ++r) {
-                pbn::ImageLayout Lr;
-                build_image(desc, Tsel, &Lr, 32 * ni.w_lo[r], std::min(desc->n, 32 * ni.w_lo[r + 1]), 32u, true,
-                            false, 0.0, true);
-                mx = std::max(mx, Lr.bytes);
-            }
-            skew = pbn::nodepar_smem_bytes(nw, 1, mx) + 64 <= (size_t)smem_optin;
-        }
         for (int r = 0; r < K; ++r) {
             pbn::ImageLayout Lr;
             const int32_t lo = 32 * ni.w_lo[r], hi = std::min(desc->n, 32 * ni.w_lo[r + 1]);
-            std::vector<uint8_t> sub = build_image(desc, Tsel, &Lr, lo, hi, 32u, true, false, 0.0, skew);
+            std::vector<uint8_t> sub = build_image(desc, Tsel, &Lr, lo, hi, 32u, true);
             const size_t off = (all.size() + 15) & ~(size_t)15;
             all.resize(off + sub.size(), 0);
             std::memcpy(all.data() + off, sub.data(), sub.size());
@@ -737,11 +719,10 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         return use;
     };
     // auto layout (cluster_size 0): lanes over nodes for few chains --
-    // measured faster than the chain-lanes kernels up to 256 chains (up to 64
-    // for n > 2048: C5 at 256 chains favours the cluster kernel K1c)
+    // measured faster than the chain-lanes kernels up to 256 chains
+    // (profiles/nodelanes_auto_r2.jsonl; at 1024 chains K1c / K1 win)
     const bool node_lanes = a->layout == PBN_LAYOUT_NODE_LANES ||
-                            (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 && a->n_chains <= 256 &&
-                             (a->n_chains <= 64 || P.n <= 2048));
+                            (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 && a->n_chains <= 256);
     const NodeParImages* np_use = nullptr;
     if (node_lanes) {
         if (a->cluster_size >= 1) {
@@ -777,9 +758,29 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         for (int r = 0; r <= np_use->K; ++r) C.w_lo[r] = np_use->w_lo[r];
         // one warp per (chain, own word) -- up to 32 warps, which then loop;
         // the geometric stream adds a warp that only draws gamma(t+1)
-        int threads = std::min(1024, 32 * (C.G * ow + (P.geometric ? 1 : 0)));
-        if (a->warps_per_group > 0) threads = std::min(1024, 32 * a->warps_per_group);
-        threads = std::max(threads, 32 * P.n_props);
+        auto threads_for = [&](int G) {
+            int t = std::min(1024, 32 * (G * ow + (P.geometric ? 1 : 0)));
+            if (a->warps_per_group > 0) t = std::min(1024, 32 * a->warps_per_group);
+            return std::max(t, 32 * P.n_props);
+        };
+        if (a->chains_per_cluster == 0) {
+            // auto G: the smallest G (from one CTA per SM upward) whose
+            // clusters all fit one wave -- clusters pack per GPC, so e.g. at
+            // most 32 clusters of 4 are resident on 148 SMs (C5, 256 chains:
+            // G = 7 -> 37 clusters, two waves, 6.3e10; G = 8 -> 1.12e11)
+            for (int G = C.G; G <= 32 && np_fits(*np_use, G); ++G) {
+                C.G = G;
+                int active = 0;
+                const int64_t clusters = (a->n_chains + G - 1) / G;
+                if (pbn::max_active_nodepar_clusters(C, threads_for(G), pbn::nodepar_smem_bytes(nw, G, np_use->max_bytes),
+                                                     &active) != 0) {
+                    cudaGetLastError();
+                    break;
+                }
+                if (clusters <= active) break;
+            }
+        }
+        const int threads = threads_for(C.G);
         const size_t smem = pbn::nodepar_smem_bytes(nw, C.G, np_use->max_bytes);
         const int rc = pbn::launch_traj_nodepar(C, threads, smem, stream);
         return rc == 0 ? PBN_OK : PBN_E_CUDA;

@@ -33,10 +33,12 @@
 //   generic descriptor (uint4)          {toff, theta, poff, 0}
 //       toff   offset of the ceil(2^theta/32) table words; poff: u32 list of
 //              state_off(parent), parents[0] first (MSB, reading Q5)
-//   PACKED form (pbn_nodepar.cu, lanes over nodes): identical, except that a
-//       parent entry a[m] (and a generic descriptor's poff list) holds the
-//       parent's NODE ID -- the state is bit-packed, node i = bit i & 31 of
-//       word i >> 5 -- and is not relocated
+//   PACKED form (pbn_nodepar.cu, lanes over nodes): the same records; a
+//       fast descriptor holds the parents as u16 NODE IDS (the state is
+//       bit-packed, node i = bit i & 31 of word i >> 5; not relocated):
+//       {t0, a[0..FT-1]} (FT <= 5, 16 bytes), {t0, t1, a[0..5]} (FT = 6),
+//       {a[0..7], table words} (FT = 7, 8) -- desc_bytes_packed(FT); a
+//       generic descriptor's poff list holds u32 node ids
 //   relocation list (u32, stored after the image in device memory, not staged)
 //       byte offsets of every image-offset-valued word above (nrec.w, thr,
 //       gdesc, toff, poff) and, flagged with kRelocState, of every fast
@@ -80,6 +82,10 @@ constexpr uint32_t kRelocState = 0x80000000u;  // relocation entry: add the stat
 // fast descriptor stride for fast width FT: t0 (+t1 when FT == 6) + FT offsets,
 // rounded up to 16 bytes
 __host__ __device__ constexpr uint32_t desc_bytes(int FT) { return FT == 3 ? 16u : FT <= 6 ? 32u : FT == 7 ? 48u : 64u; }
+// the same for the PACKED image (lanes over nodes): u16 parent ids --
+// {t0, a[0..FT-1]} in one 16-byte chunk for FT <= 5, {t0, t1, a[0..5]} for
+// FT = 6, {a[0..7], 2^FT / 32 table words} for FT = 7, 8
+__host__ __device__ constexpr uint32_t desc_bytes_packed(int FT) { return FT <= 5 ? 16u : FT <= 7 ? 32u : 48u; }
 // byte offset of node i's word in buffer 0 of the group state
 // (qs = bytes between quads: 32 for two interleaved buffers, 48 for three)
 __host__ __device__ constexpr uint32_t state_off(uint32_t i, uint32_t qs = 32) { return qs * (i >> 2) + 4u * (i & 3u); }

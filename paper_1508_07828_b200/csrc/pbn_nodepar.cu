@@ -36,6 +36,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "pbn_internal.h"
 #include "pbn_node.cuh"
@@ -103,47 +106,38 @@ __device__ __forceinline__ uint32_t pbit(uint32_t S, uint32_t p)
     return __funnelshift_r(w, w, p) & 1u;  // wrap mode: rotate right by p mod 32
 }
 
-// A6 for one fast function of the packed image: descriptor at dp, parents
-// are node ids, MSB first (reading Q5); returns the new bit
+// A6 for one fast function of the packed image (desc_bytes_packed layout,
+// u16 parent node ids, MSB first, reading Q5): returns the new bit
+__device__ __forceinline__ uint32_t u16of(const uint32_t* pairs, int m)
+{
+    return (m & 1) ? pairs[m >> 1] >> 16 : pairs[m >> 1] & 0xFFFFu;
+}
 template <int FT>
-__device__ __forceinline__ uint32_t fast_bit_packed(uint32_t dp, uint32_t S, uint32_t ibase)
+__device__ __forceinline__ uint32_t fast_bit_packed(uint32_t dp, uint32_t S)
 {
     uint32_t tw, idx = 0;
+    const uint4 d0 = lds128_ro(dp);
     if constexpr (FT >= 7) {
-        // {a[0..7], table words}: the first FT-5 parents pick the table word;
-        // FT = 8: 16-byte chunk c stored at chunk c ^ sw, sw = the descriptor's
-        // 64-byte index mod 4 within the sub-image (bank spread, build_image)
-        const uint32_t sw = FT == 8 ? ((dp - ibase) >> 6) & 3u : 0u;
-        const uint4 d0 = lds128_ro(dp + 16u * (0u ^ sw)), d1 = lds128_ro(dp + 16u * (1u ^ sw));
-        const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        // {a[0..7] as u16, table words}: the first FT-5 parents pick the table word
+        const uint32_t pr[4] = {d0.x, d0.y, d0.z, d0.w};
         uint32_t widx = 0;
 #pragma unroll
-        for (int m = 0; m < FT - 5; ++m) widx = 2u * widx + pbit(S, a[m]);
+        for (int m = 0; m < FT - 5; ++m) widx = 2u * widx + pbit(S, u16of(pr, m));
 #pragma unroll
-        for (int m = FT - 5; m < FT; ++m) idx = 2u * idx + pbit(S, a[m]);
-        tw = FT == 8 ? lds32_ro(dp + 16u * ((2u + (widx >> 2)) ^ sw) + 4u * (widx & 3u))
-                     : lds32_ro(dp + 32u + 4u * widx);
+        for (int m = FT - 5; m < FT; ++m) idx = 2u * idx + pbit(S, u16of(pr, m));
+        tw = lds32_ro(dp + 16u + 4u * widx);
+    } else if constexpr (FT == 6) {
+        // {t0, t1, a[0..5] as u16}
+        const uint32_t pr[3] = {d0.z, d0.w, lds32_ro(dp + 16u)};
+        tw = pbit(S, u16of(pr, 0)) ? d0.y : d0.x;
+#pragma unroll
+        for (int m = 1; m < 6; ++m) idx = 2u * idx + pbit(S, u16of(pr, m));
     } else {
-        // {t0, [t1], a[0..FT-1]}
-        const uint4 d0 = lds128_ro(dp);
-        uint32_t a[6] = {0, 0, 0, 0, 0, 0};
-        uint32_t t0 = d0.x, t1 = 0;
-        if (FT == 6) {
-            const uint4 d1 = lds128_ro(dp + 16u);
-            t1 = d0.y;
-            a[0] = d0.z, a[1] = d0.w, a[2] = d1.x, a[3] = d1.y, a[4] = d1.z, a[5] = d1.w;
-        } else if (FT == 5) {
-            const uint2 d1 = lds64_ro(dp + 16u);
-            a[0] = d0.y, a[1] = d0.z, a[2] = d0.w, a[3] = d1.x, a[4] = d1.y;
-        } else if (FT == 4) {
-            a[0] = d0.y, a[1] = d0.z, a[2] = d0.w, a[3] = lds32_ro(dp + 16u);
-        } else {
-            a[0] = d0.y, a[1] = d0.z, a[2] = d0.w;
-        }
-        constexpr int S0 = FT == 6 ? 1 : 0;
-        tw = (FT == 6 && pbit(S, a[0])) ? t1 : t0;
+        // {t0, a[0..FT-1] as u16}
+        const uint32_t pr[3] = {d0.y, d0.z, d0.w};
+        tw = d0.x;
 #pragma unroll
-        for (int m = S0; m < FT; ++m) idx = 2u * idx + pbit(S, a[m]);
+        for (int m = 0; m < FT; ++m) idx = 2u * idx + pbit(S, u16of(pr, m));
     }
     // table words are stored bit-reversed: the entry is the sign bit of tw << idx
     return (uint32_t)((int32_t)(tw << idx) < 0);
@@ -358,11 +352,11 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
             if (!SLOW || (rec.w & 7u) != kSlowNode) {
                 // A5: function j = #{k : u > E_k}
                 uint32_t dp = rec.w;
-                constexpr uint32_t DS = desc_bytes(FT);
+                constexpr uint32_t DS = desc_bytes_packed(FT);
                 if (u > rec.x) dp += DS;
                 if (u > rec.y) dp += DS;
                 if (u > rec.z) dp += DS;
-                bit = fast_bit_packed<FT>(dp, So, ibase);
+                bit = fast_bit_packed<FT>(dp, So);
             } else {
                 bit = slow_bit_packed(rec.w, u, So);
             }
@@ -493,11 +487,27 @@ int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, 
 int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem_bytes, int* out)
 {
     const void* fn = npick(C);
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+    const auto key = std::make_tuple(fn, (int)C.K, threads, smem_bytes);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *out = it->second;
+            return 0;
+        }
+    }
     cudaError_t e = nprepare(fn, C, smem_bytes);
     if (e != cudaSuccess) return (int)e;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = ncfg(C, threads, smem_bytes, (unsigned)C.K, attr);
-    return (int)cudaOccupancyMaxActiveClusters(out, fn, &cfg);
+    const cudaError_t r = cudaOccupancyMaxActiveClusters(out, fn, &cfg);
+    if (r == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = *out;
+    }
+    return (int)r;
 }
 
 }  // namespace pbn
