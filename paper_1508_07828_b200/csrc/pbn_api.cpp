@@ -768,8 +768,9 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
             // clusters all fit one wave -- clusters pack per GPC, so e.g. at
             // most 32 clusters of 4 are resident on 148 SMs (C5, 256 chains:
             // G = 7 -> 37 clusters, two waves, 6.3e10; G = 8 -> 1.12e11)
-            for (int G = C.G; G <= 32 && np_fits(*np_use, G); ++G) {
+                for (int G = C.G; G <= 32 && np_fits(*np_use, G); ++G) {
                 C.G = G;
+                C.share = (int)(G * ow > threads_for(G) / 32);
                 int active = 0;
                 const int64_t clusters = (a->n_chains + G - 1) / G;
                 if (pbn::max_active_nodepar_clusters(C, threads_for(G), pbn::nodepar_smem_bytes(nw, G, np_use->max_bytes),
@@ -781,6 +782,8 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
             }
         }
         const int threads = threads_for(C.G);
+        // warps with >= 2 (chain, word) items per step share Philox calls
+        C.share = (int)(C.G * ow > threads / 32);
         const size_t smem = pbn::nodepar_smem_bytes(nw, C.G, np_use->max_bytes);
         const int rc = pbn::launch_traj_nodepar(C, threads, smem, stream);
         return rc == 0 ? PBN_OK : PBN_E_CUDA;

@@ -186,6 +186,7 @@ struct NodeParParams {
     int32_t w_lo[kMaxCluster + 1];
     const uint32_t* geo_table;  // geometric mode: Cg[0..n-1] in global memory (the full image's copy)
     uint32_t geo_last;          // Cg[n-1]: gamma(t) != 0 iff the first skip word is below it
+    int32_t share;              // kernel variant: Philox calls shared by shuffles (>= 2 items per warp)
 };
 size_t nodepar_smem_bytes(int n_words, int G, uint32_t max_sub_image);
 int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, void* stream);

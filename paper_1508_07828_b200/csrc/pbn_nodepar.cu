@@ -165,7 +165,10 @@ __device__ __noinline__ uint32_t slow_bit_packed(uint32_t w, uint32_t u, uint32_
 // (any flip <=> the first skip word is below Cg[n-1]; the flip positions by
 // skips over the image's table in global memory) into flip words Gm; a chain
 // with gamma != 0 takes s XOR gamma, so its node evaluation is skipped.
-template <int MODE, int FT, bool SLOW>
+// SHARE: a warp has >= 2 items per step, so quads' Philox calls are shared
+// through shuffles (batches of up to 4 items); else one call per lane (the
+// shuffles would only lengthen the latency chain of a lone item)
+template <int MODE, int FT, bool SLOW, bool SHARE>
 __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_constant__ NodeParParams C)
 {
     constexpr bool PER_NODE = MODE == 1;
@@ -320,16 +323,10 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
         if (GEO && r < total)
             for (int g = NWARP - 1 - wg; g >= 0 && g < Ge; g += NWARP) geo_draw(g, t + 1, par ^ 1u);
         // ---- A3-A6: warp = (chain g, own word j), lane = node 32 j + lane ----
-        // (items it = g OW + (j - w_lo) strided by the warp count, walked
-        // without integer division)
-        int g = wg / OW, jj = wg % OW;
-        for (int it = wg; it < Ge * OW; it += NWARP, jj += NWARP) {
-            while (jj >= OW) {
-                jj -= OW;
-                ++g;
-            }
-            const int j = w_lo + jj;
-            const uint32_t chain = (uint32_t)(P.chain_base + chain0 + g);
+        // Items it = g OW + (j - w_lo), strided by the warp count and walked
+        // without integer division.
+        // one (chain g, word j) item with the 4 words of this lane's quad
+        auto item = [&](int g, int j, uint32_t ux, uint32_t uy, uint32_t uz, uint32_t uw) {
             const uint32_t a = Xp(par, g) + 8u * (uint32_t)j;
             if (GEO && lds32(Gfp(par, g))) {
                 // gamma(t) != 0: s_t = s_{t-1} XOR gamma, applied by
@@ -337,15 +334,13 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
                 if (lane == 0) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(0u), "r"(0u) : "memory");
                 if (lane < (int)K && lane != (int)rank)
                     st_async_v2(np_map_peer(a, (uint32_t)lane), 0u, 0u, np_map_peer(bar, (uint32_t)lane));
-                continue;
+                return;
             }
             const uint32_t So = Sp(par ^ 1u, g);
             const uint32_t i = 32u * (uint32_t)j + (uint32_t)lane;
             const bool live = (int)i < n;
             const uint32_t ic = live ? i : node_lo;  // lanes past the last node read a valid record
-            // A3: the quad's Philox call (the quad's 4 lanes compute the same call)
-            const uint4 rw = philox4x32_10(ic >> 2, chain, (uint32_t)t, (uint32_t)(t >> 32), P.rk);
-            const uint32_t u = (ic & 2u) ? ((ic & 1u) ? rw.w : rw.z) : ((ic & 1u) ? rw.y : rw.x);
+            const uint32_t u = (i & 2u) ? ((i & 1u) ? uw : uz) : ((i & 1u) ? uy : ux);
             const uint4 rec = lds128_ro(ibase + 16u * (ic - node_lo));
             const uint32_t gm = u < Tp ? 1u : 0u;  // gamma_i(t) (A4)
             uint32_t bit;
@@ -368,6 +363,59 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
             if (lane == 0) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(vf), "r"(vg) : "memory");
             if (lane < (int)K && lane != (int)rank)
                 st_async_v2(np_map_peer(a, (uint32_t)lane), vf, vg, np_map_peer(bar, (uint32_t)lane));
+        };
+        int g = wg / OW, jj = wg % OW;
+        if constexpr (!SHARE) {
+            // one item per warp and step: each lane computes its quad's call
+            for (int it = wg; it < Ge * OW; it += NWARP, jj += NWARP) {
+                while (jj >= OW) {
+                    jj -= OW;
+                    ++g;
+                }
+                const int j = w_lo + jj;
+                const uint32_t i = 32u * (uint32_t)j + (uint32_t)lane;
+                const uint32_t q = min(i >> 2, (uint32_t)P.nquads - 1u);
+                const uint4 rw = philox4x32_10(q, (uint32_t)(P.chain_base + chain0 + g), (uint32_t)t,
+                                               (uint32_t)(t >> 32), P.rk);
+                item(g, j, rw.x, rw.y, rw.z, rw.w);
+            }
+        } else {
+            // batches of up to 4 items: lane l computes the call of quad l & 7
+            // of item l >> 3 (32 distinct calls), node lanes take their words
+            // by shuffles -- one call per quad instead of one per node
+            const int BATCH = min(4, (Ge * OW + NWARP - 1) / NWARP);
+            for (int it0 = wg; it0 < Ge * OW; it0 += BATCH * NWARP) {
+                int gk[4], jk[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k > 0 && k < BATCH) jj += NWARP;
+                    while (jj >= OW) {
+                        jj -= OW;
+                        ++g;
+                    }
+                    gk[k] = g;
+                    jk[k] = w_lo + jj;
+                }
+                jj += NWARP;  // the next batch starts one stride after its last item
+                const int nk = min(BATCH, (Ge * OW - it0 + NWARP - 1) / NWARP);  // items in this batch
+                uint4 rw;
+                {
+                    const int k = lane >> 3;
+                    const int gg = k == 0 ? gk[0] : k == 1 ? gk[1] : k == 2 ? gk[2] : gk[3];
+                    const int jq = k == 0 ? jk[0] : k == 1 ? jk[1] : k == 2 ? jk[2] : jk[3];
+                    const uint32_t q = min(8u * (uint32_t)jq + (uint32_t)(lane & 7), (uint32_t)P.nquads - 1u);
+                    rw = philox4x32_10(q, (uint32_t)(P.chain_base + chain0 + gg), (uint32_t)t, (uint32_t)(t >> 32),
+                                       P.rk);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k >= nk) break;
+                    const int src = 8 * k + (lane >> 2);  // the quad's call: lane 8 k + quad-in-word
+                    const uint32_t ux = __shfl_sync(FULL, rw.x, src), uy = __shfl_sync(FULL, rw.y, src);
+                    const uint32_t uz = __shfl_sync(FULL, rw.z, src), uw = __shfl_sync(FULL, rw.w, src);
+                    item(gk[k], jk[k], ux, uy, uz, uw);
+                }
+            }
         }
         // ---- wait for every peer's words of this step: one warp spins on the
         // mbarrier, the others wait in the CTA barrier (spinning warps would
@@ -418,21 +466,22 @@ __global__ void __launch_bounds__(1024, 1) traj_nodepar_kernel(const __grid_cons
 }
 
 template <int MODE, int FT, bool SLOW>
-const void* nkptr()
+const void* nkptr(bool share)
 {
-    return reinterpret_cast<const void*>(&traj_nodepar_kernel<MODE, FT, SLOW>);
+    return share ? reinterpret_cast<const void*>(&traj_nodepar_kernel<MODE, FT, SLOW, true>)
+                 : reinterpret_cast<const void*>(&traj_nodepar_kernel<MODE, FT, SLOW, false>);
 }
 
 template <int MODE>
-const void* npick_ft(int FT, bool slow)
+const void* npick_ft(int FT, bool slow, bool share)
 {
     switch (FT) {
-        case 3: return slow ? nkptr<MODE, 3, true>() : nkptr<MODE, 3, false>();
-        case 4: return slow ? nkptr<MODE, 4, true>() : nkptr<MODE, 4, false>();
-        case 5: return slow ? nkptr<MODE, 5, true>() : nkptr<MODE, 5, false>();
-        case 6: return slow ? nkptr<MODE, 6, true>() : nkptr<MODE, 6, false>();
-        case 7: return slow ? nkptr<MODE, 7, true>() : nkptr<MODE, 7, false>();
-        default: return slow ? nkptr<MODE, 8, true>() : nkptr<MODE, 8, false>();
+        case 3: return slow ? nkptr<MODE, 3, true>(share) : nkptr<MODE, 3, false>(share);
+        case 4: return slow ? nkptr<MODE, 4, true>(share) : nkptr<MODE, 4, false>(share);
+        case 5: return slow ? nkptr<MODE, 5, true>(share) : nkptr<MODE, 5, false>(share);
+        case 6: return slow ? nkptr<MODE, 6, true>(share) : nkptr<MODE, 6, false>(share);
+        case 7: return slow ? nkptr<MODE, 7, true>(share) : nkptr<MODE, 7, false>(share);
+        default: return slow ? nkptr<MODE, 8, true>(share) : nkptr<MODE, 8, false>(share);
     }
 }
 
@@ -440,7 +489,8 @@ const void* npick(const NodeParParams& C)
 {
     const int FT = C.T.L.fast_theta;
     const bool slow = C.T.L.slow_nodes > 0;
-    return C.T.per_node ? npick_ft<1>(FT, slow) : C.T.geometric ? npick_ft<2>(FT, slow) : npick_ft<0>(FT, slow);
+    return C.T.per_node ? npick_ft<1>(FT, slow, C.share)
+                        : C.T.geometric ? npick_ft<2>(FT, slow, C.share) : npick_ft<0>(FT, slow, C.share);
 }
 
 cudaLaunchConfig_t ncfg(const NodeParParams& C, int threads, size_t smem, unsigned grid, cudaLaunchAttribute* attr)
