@@ -189,6 +189,27 @@ struct Img {
         if (SMEM) return lds16_ro(a);
         return (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(gbase + a));
     }
+    // a + OFF with OFF a compile-time byte offset: the global path forms the
+    // 64-bit address of a once and folds OFF into the load's immediate (a
+    // 32-bit a + OFF first would cost an add and a 64-bit extension per load)
+    template <uint32_t OFF>
+    __device__ __forceinline__ uint4 ld128(uint32_t a) const
+    {
+        if (SMEM) return lds128_ro(a + OFF);
+        return __ldg(reinterpret_cast<const uint4*>(gbase + a + OFF));
+    }
+    template <uint32_t OFF>
+    __device__ __forceinline__ uint2 ld64(uint32_t a) const
+    {
+        if (SMEM) return lds64_ro(a + OFF);
+        return __ldg(reinterpret_cast<const uint2*>(gbase + a + OFF));
+    }
+    template <uint32_t OFF>
+    __device__ __forceinline__ uint32_t ld32(uint32_t a) const
+    {
+        if (SMEM) return lds32_ro(a + OFF);
+        return __ldg(reinterpret_cast<const uint32_t*>(gbase + a + OFF));
+    }
 };
 
 // Generic path for nodes outside the fast shape (ell > 4 or theta_max > 8:
@@ -263,7 +284,7 @@ __device__ __forceinline__ uint32_t fast_bit(const Img<SMEM>& img, const uint32_
         // pick one of the 2^(FT-5) table words (a dependent load), the other
         // five index within it
         const uint4 d0 = img.ld128(dp);
-        const uint4 d1 = img.ld128(dp + 16u);
+        const uint4 d1 = img.template ld128<16u>(dp);
         const uint32_t a[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
         constexpr int S = FT >= 7 ? FT - 5 : 2;
         uint32_t widx = 0;
@@ -275,7 +296,7 @@ __device__ __forceinline__ uint32_t fast_bit(const Img<SMEM>& img, const uint32_
         add_if_bit<4u>(idx, lds32_state(SB(a[(S + 2) % 8]) + OB), lmask);
         add_if_bit<2u>(idx, lds32_state(SB(a[(S + 3) % 8]) + OB), lmask);
         add_if_bit<1u>(idx, lds32_state(SB(a[(S + 4) % 8]) + OB), lmask);
-        tw = img.ld32(dp + 32u + widx);
+        tw = img.template ld32<32u>(dp + widx);
     } else {
     // descriptor words {t0, [t1], a[0..FT-1]}: table word(s), then the FT
     // padded parents' state offsets, MSB first
@@ -283,14 +304,14 @@ __device__ __forceinline__ uint32_t fast_bit(const Img<SMEM>& img, const uint32_
     {
         const uint4 d0 = img.ld128(dp);
         if (FT == 6) {
-            const uint4 d1 = img.ld128(dp + 16u);
+            const uint4 d1 = img.template ld128<16u>(dp);
             tw0 = d0.x; tw1 = d0.y; a[0] = d0.z; a[1] = d0.w;
             a[2] = d1.x; a[3] = d1.y; a[4] = d1.z; a[5] = d1.w;
         } else if (FT == 5) {
-            const uint2 d1 = img.ld64(dp + 16u);
+            const uint2 d1 = img.template ld64<16u>(dp);
             tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1.x; a[4] = d1.y; a[5] = 0;
         } else if (FT == 4) {
-            const uint32_t d1 = img.ld32(dp + 16u);
+            const uint32_t d1 = img.template ld32<16u>(dp);
             tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = d1; a[4] = a[5] = 0;
         } else {
             tw0 = d0.x; a[0] = d0.y; a[1] = d0.z; a[2] = d0.w; a[3] = a[4] = a[5] = 0;

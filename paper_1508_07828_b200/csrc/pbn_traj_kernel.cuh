@@ -81,7 +81,10 @@ __global__ void __launch_bounds__(SMEM ? PBN_MAX_THREADS : kGlobalImageThreads, 
     const int n = P.n;
     // dynamic shared memory: [group state | gamma words | any words] then the
     // staged image (16-aligned) -- the state sits at the window's dynamic base
-    const uint32_t gbase = smem_u32(smem);                   // state base
+    // state base; the global-image kernels add it to every parent offset, so
+    // it is made a uniform value (redux: UR) and the adds fold into the LDS
+    // address ([R + UR]) -- from the symbol, ptxas rematerialises it per use
+    const uint32_t gbase = SMEM ? smem_u32(smem) : __reduce_or_sync(FULL, smem_u32(smem));
     const uint32_t sbase = gbase + 4u * (uint32_t)P.group_words;  // image base
 
     // ---- A1: stage the model image into shared memory (bulk async copy) ----

@@ -9,8 +9,10 @@ key = sys.argv[1] if len(sys.argv) > 1 else "C5"
 model, pred = config_model(key), config_predicate(key)
 pm = pbn.pbn_load(model)
 steps = 2000
-for chains in (1, 64, 1024):
-    for K in (1, 2, 4, 8, 16):
+chain_list = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 64, 1024]
+Ks = [int(c) for c in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4, 8, 16]
+for chains in chain_list:
+    for K in Ks:
         if K > (model.n + 3) // 4:
             continue
         out = pbn.alloc_outputs(pm, chains, steps, batch=100, emit_bits=True)
