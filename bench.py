@@ -371,6 +371,8 @@ def main():
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=0, help="0 auto, 1 CTA per group, 2 persistent")
     ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
+    ap.add_argument("--layout", type=int, default=0,
+                    help="PBN_LAYOUT_*: 0 auto, 1 chain lanes (K1/K1c), 2 node lanes (K1n), 3 bit-sliced (K1b)")
     ap.add_argument("--sweep", action="store_true", help="C5 chain-count sweep (one line per count)")
     ap.add_argument("--e2e-steps", type=int, default=3, help="timed end-to-end (host buffer) iterations")
     ap.add_argument("--protocol", default="",
@@ -423,7 +425,7 @@ def main():
         pbn.pbn_simulate(pm, out, n_chains=chains, chain_base=chain_base, steps=window,
                          burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=True,
                          emit_bits=True, groups_per_cta=args.groups, warps_per_group=args.warps,
-                         schedule=args.schedule, chunk_steps=args.chunk,
+                         schedule=args.schedule, chunk_steps=args.chunk, layout=args.layout,
                          stream=stream)
 
     for _ in range(args.warmup):
@@ -500,7 +502,7 @@ def main():
             out.state.copy_(host_state, non_blocking=True)
             pbn.pbn_simulate(pm, out, n_chains=chains, chain_base=chain_base, steps=window,
                              burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=False,
-                             emit_bits=True, stream=stream)
+                             emit_bits=True, warps_per_group=args.warps, layout=args.layout, stream=stream)
             for k, t in res_host.items():
                 t.copy_(getattr(out, k), non_blocking=True)
 

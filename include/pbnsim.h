@@ -198,8 +198,11 @@ typedef struct {
 enum {
     PBN_LAYOUT_AUTO = 0,        /* chosen per call from the chain count and image size  */
     PBN_LAYOUT_CHAIN_LANES = 1, /* 32 chains per warp, bit-sliced state (K1, K1c)       */
-    PBN_LAYOUT_NODE_LANES = 2   /* one chain per cluster of cluster_size CTAs (0 = auto), */
+    PBN_LAYOUT_NODE_LANES = 2,  /* one chain per cluster of cluster_size CTAs (0 = auto), */
                                 /* threads over node quads, bit-packed state (K1n)     */
+    PBN_LAYOUT_BITSLICE = 3     /* K1's group layout, functions evaluated bit-sliced    */
+                                /* over the 32 chains (K1b); models with theta <= 6,    */
+                                /* ell <= 4 and VECTOR / PER_NODE semantics only        */
 };
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).

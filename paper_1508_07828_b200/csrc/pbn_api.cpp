@@ -103,6 +103,11 @@ struct pbn_model_s {
     int64_t n_parents = 0;
     std::vector<ClusterImages> clusters;  // K = 2, 4, 8, 16 (K <= quads)
     std::vector<NodeParImages> nodepar;   // K = 1, 2, 4, 8, 16 (K <= packed words)
+    // bit-sliced evaluation image (K1b), when every function has <= 6 parents
+    // and every node <= 4 functions (pbn_internal.h)
+    uint8_t* d_bs = nullptr;
+    uint32_t bs_bytes = 0, bs_erec_off = 0, bs_rounds_off = 0;
+    int32_t bs_rounds = 0, bs_L = 0;
     uint32_t geo_last = 0;                // geometric mode: Cg[n-1]
     uint32_t geo_off = 0;                 // geometric mode: byte offset of Cg in the image
     double p = 0.0;
@@ -440,6 +445,99 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
     return B.buf;
 }
 
+// BITSLICE image (layout: pbn_internal.h): per-quad selection thresholds,
+// function tasks grouped by class c = max(theta, 1) in whole rounds of 32,
+// and the round list (most expensive class first).  Returns false when the
+// model is outside the bit-sliced kernel's shape (theta > 6, ell > 4, too
+// many nodes for u16 offsets).
+bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint8_t>& out, uint32_t* erec_off,
+                          uint32_t* rounds_off, int32_t* n_rounds, int32_t* L_out)
+{
+    const int32_t n = d->n;
+    if (n > pbn::kBitsliceMaxNodes) return false;
+    int32_t L = 1;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t ell = d->fn_off[i + 1] - d->fn_off[i];
+        if (ell > pbn::kBitsliceMaxEll) return false;
+        L = std::max(L, ell);
+        for (int32_t f = d->fn_off[i]; f < d->fn_off[i + 1]; ++f)
+            if (d->par_off[f + 1] - d->par_off[f] > pbn::kBitsliceMaxTheta) return false;
+    }
+    const int32_t nq = (n + 3) / 4;
+    ImageBuilder B;
+    // thresholds E_1..E_{L-1} per quad, plane-major: [q][m] = {E_{m+1} of nodes 4q..4q+3}
+    const uint32_t eo = B.alloc(16u * (size_t)std::max(nq * (L - 1), 1));
+    for (int32_t i = 0; i < 4 * nq; ++i) {
+        std::vector<uint32_t> E;
+        if (i < n) {
+            const int32_t f0 = d->fn_off[i], ell = d->fn_off[i + 1] - f0;
+            double cum = 0.0;
+            for (int32_t j = 0; j + 1 < ell; ++j) {
+                cum += d->sel_prob[f0 + j];
+                E.push_back(boundary_E(cum, Tp));
+            }
+        }
+        for (int32_t m = 0; m + 1 < L; ++m)
+            B.u32(eo + 16u * (uint32_t)((i >> 2) * (L - 1) + m))[i & 3] = m < (int32_t)E.size() ? E[m] : 0xFFFFFFFFu;
+    }
+    // tasks by class
+    std::vector<std::pair<int32_t, int32_t>> cls[pbn::kBitsliceMaxTheta + 1];  // (node, j)
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t f = d->fn_off[i]; f < d->fn_off[i + 1]; ++f)
+            cls[std::max(d->par_off[f + 1] - d->par_off[f], 1)].push_back({i, f - d->fn_off[i]});
+    std::vector<std::pair<uint32_t, uint32_t>> rounds;  // (task offset, class)
+    for (int32_t c = pbn::kBitsliceMaxTheta; c >= 1; --c) {
+        if (cls[c].empty()) continue;
+        const uint32_t stride = c == 6 ? 32u : 16u;
+        const size_t cnt = (cls[c].size() + 31) & ~(size_t)31;
+        const uint32_t to = B.alloc(stride * cnt, 16);
+        for (size_t k = 0; k < cnt; ++k) {
+            uint32_t* w = B.u32(to + stride * (uint32_t)k);
+            if (k >= cls[c].size()) {  // dummy task: table 0 contributes nothing
+                w[c == 6 ? 2 : 1] = 1u;  // node 0, function 1 (no perturbation term)
+                continue;
+            }
+            const int32_t i = cls[c][k].first, j = cls[c][k].second, f = d->fn_off[i] + j;
+            const int32_t theta = d->par_off[f + 1] - d->par_off[f];
+            // table padded to c index bits: padding parents are the low bits
+            uint32_t T[2] = {0u, 0u};
+            for (uint32_t e = 0; e < (1u << c); ++e)
+                T[e >> 5] |= table_bit(d, f, e >> (c - theta)) << (e & 31u);
+            uint32_t p[6] = {0, 0, 0, 0, 0, 0};
+            for (int32_t m = 0; m < c; ++m)
+                p[m] = pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u);
+            const uint32_t ij = ((uint32_t)i << 2) | (uint32_t)j;
+            if (c <= 5) {
+                w[0] = T[0];
+                w[1] = ij | (p[0] << 16);
+                w[2] = p[1] | (p[2] << 16);
+                w[3] = p[3] | (p[4] << 16);
+            } else {
+                w[0] = T[0];
+                w[1] = T[1];
+                w[2] = ij | (p[0] << 16);
+                w[3] = p[1] | (p[2] << 16);
+                w[4] = p[3] | (p[4] << 16);
+                w[5] = p[5];
+            }
+        }
+        for (size_t k = 0; k < cnt; k += 32) rounds.push_back({to + stride * (uint32_t)k, (uint32_t)c});
+    }
+    const uint32_t ro = B.alloc(8u * std::max<size_t>(rounds.size(), 1), 16);
+    for (size_t r = 0; r < rounds.size(); ++r) {
+        B.u32(ro)[2 * r] = rounds[r].first;
+        B.u32(ro)[2 * r + 1] = rounds[r].second;
+    }
+    B.alloc(16);
+    B.buf.resize((B.buf.size() + 15) & ~(size_t)15);
+    out.swap(B.buf);
+    *erec_off = eo;
+    *rounds_off = ro;
+    *n_rounds = (int32_t)rounds.size();
+    *L_out = L;
+    return true;
+}
+
 pbn_status cuda_status(cudaError_t e, char* err, size_t errlen, const char* what)
 {
     if (e == cudaSuccess) return PBN_OK;
@@ -503,6 +601,21 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
         delete m;
         return cuda_status(e, err, errlen, "cudaMemcpy(image)");
     }
+    // bit-sliced evaluation image (K1b; VECTOR and PER_NODE semantics)
+    if (!geo) {
+        std::vector<uint8_t> bs;
+        if (build_bitslice_image(desc, m->Tp, bs, &m->bs_erec_off, &m->bs_rounds_off, &m->bs_rounds, &m->bs_L)) {
+            if (cudaMalloc(&m->d_bs, bs.size()) != cudaSuccess ||
+                cudaMemcpy(m->d_bs, bs.data(), bs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+                if (m->d_bs) cudaFree(m->d_bs);
+                cudaFree(m->d_image);
+                delete m;
+                set_err(err, errlen, "bitslice image upload failed");
+                return PBN_E_CUDA;
+            }
+            m->bs_bytes = (uint32_t)bs.size();
+        }
+    }
     // sub-images for the cluster kernel: CTA r of a K-cluster owns quads
     // [Q r / K, Q (r+1) / K) and its nodes' records and descriptors
     const int32_t nq = (desc->n + 3) / 4;
@@ -530,6 +643,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
             cudaMemcpy(ci.d_buf, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
             if (ci.d_buf) cudaFree(ci.d_buf);
             for (auto& c : m->clusters) cudaFree(c.d_buf);
+            if (m->d_bs) cudaFree(m->d_bs);
             cudaFree(m->d_image);
             delete m;
             set_err(err, errlen, "cluster sub-image upload failed");
@@ -563,6 +677,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
             if (ni.d_buf) cudaFree(ni.d_buf);
             for (auto& c : m->nodepar) cudaFree(c.d_buf);
             for (auto& c : m->clusters) cudaFree(c.d_buf);
+            if (m->d_bs) cudaFree(m->d_bs);
             cudaFree(m->d_image);
             delete m;
             set_err(err, errlen, "node-parallel sub-image upload failed");
@@ -578,6 +693,7 @@ void pbn_free(pbn_model model)
 {
     if (!model) return;
     if (model->d_image) cudaFree(model->d_image);
+    if (model->d_bs) cudaFree(model->d_bs);
     for (auto& c : model->clusters) cudaFree(c.d_buf);
     for (auto& c : model->nodepar) cudaFree(c.d_buf);
     delete model;
@@ -672,6 +788,47 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
     return PBN_OK;
 }
 
+// K1b launch: one 32-chain group per CTA (persistent schedule as K1), the
+// bitslice image staged into shared memory.  PBN_E_USAGE when the model has
+// no bitslice image (theta > 6, ell > 4, geometric mode) or it does not fit.
+static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const pbn_sim_args* a, void* stream,
+                                    int smem_optin)
+{
+    if (!m->d_bs) return PBN_E_USAGE;
+    pbn::BitsliceParams Bp;
+    std::memset(&Bp, 0, sizeof(Bp));
+    Bp.T = P;
+    Bp.T.image = m->d_bs;
+    Bp.T.group_words = pbn::bitslice_group_words(P.n_pad, m->bs_L);
+    Bp.T.image_smem_bytes = m->bs_bytes;
+    Bp.erec_off = m->bs_erec_off;
+    Bp.rounds_off = m->bs_rounds_off;
+    Bp.n_rounds = m->bs_rounds;
+    Bp.any_off = 8 * P.n_pad;
+    Bp.sel_off = 8 * P.n_pad + 128;
+    int W = a->warps_per_group > 0 ? a->warps_per_group : pbn::default_group_warps(P.nquads);
+    W = std::max(W, P.n_props);
+    if (W > pbn::kMaxWarpsPerCta || W > std::max(P.nquads, P.n_props)) return PBN_E_USAGE;
+    pbn::LaunchPlan plan;
+    plan.warps_per_group = W;
+    plan.node_warps = std::min(W, P.nquads);
+    plan.stats_warp0 = 0;
+    plan.ctas = (int)((P.n_chains + 31) / 32);
+    plan.threads = 32 * W;
+    plan.smem_bytes = (size_t)Bp.T.group_words * 4 + m->bs_bytes;
+    plan.image_in_smem = true;
+    if (plan.smem_bytes + 64 > (size_t)smem_optin) return PBN_E_USAGE;
+    Bp.T.warps_per_group = W;
+    Bp.T.node_warps = plan.node_warps;
+    Bp.T.stats_warp0 = 0;
+    if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0 || a->workspace_bytes < 0) return PBN_E_USAGE;
+    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : 0, m->bs_L);
+    const int rc = pbn::launch_group_units(Bp.T, fn, &Bp, plan, m->device, a->schedule, a->chunk_steps, a->workspace,
+                                           (size_t)a->workspace_bytes, stream);
+    if (rc == -2) return PBN_E_USAGE;
+    return rc == 0 ? PBN_OK : PBN_E_CUDA;
+}
+
 pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o, void* stream)
 {
     pbn::TrajParams P;
@@ -690,7 +847,11 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     if (smem_optin <= 0 || sms <= 0) return PBN_E_CUDA;
     const size_t limit = (size_t)smem_optin - 64;
     const int64_t groups = (a->n_chains + 31) / 32;
-    if (a->layout < PBN_LAYOUT_AUTO || a->layout > PBN_LAYOUT_NODE_LANES) return PBN_E_USAGE;
+    if (a->layout < PBN_LAYOUT_AUTO || a->layout > PBN_LAYOUT_BITSLICE) return PBN_E_USAGE;
+    if (a->layout == PBN_LAYOUT_BITSLICE) {
+        if (a->cluster_size > 1 || a->chains_per_cluster != 0) return PBN_E_USAGE;
+        return simulate_bitslice(m, P, a, stream, smem_optin);
+    }
     // ---- lanes over nodes (K1n): G chains per cluster of K CTAs ----
     const int32_t nw = (P.n + 31) / 32;
     if (a->chains_per_cluster < 0 || a->chains_per_cluster > 32) return PBN_E_USAGE;

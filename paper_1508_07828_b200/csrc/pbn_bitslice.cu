@@ -1,0 +1,411 @@
+// pbn_bitslice.cu -- K1b: the fused PBN trajectory kernel with BIT-SLICED
+// function evaluation (sm_100a).
+//
+// The same hot path as K1 (§2.2) on
+// the same group layout -- one 32-chain group per CTA, its state bit-sliced
+// in shared memory (word i = node i of the 32 chains, bit l = chain of lane
+// l, two interleaved buffers, pbn_internal.h) -- but the node step is split
+// in two phases so that the truth-table work is done once per 32 chains
+// instead of once per chain:
+//
+//   phase A (lane = chain; every warp its quads of nodes, as K1):
+//     one Philox4x32-10 call per quad (A3, reading Q2); per node the
+//     selection planes s_m = ballot(u > E_m), m = 1..L-1 (A5: chain l picks
+//     function j = #{m : u_l > E_m}, so bit l of s_j & ~s_{j+1} is set iff
+//     chain l picks j); one vote per quad flags the ~1 % of quads where some
+//     chain drew u < T_p, whose gamma words (A4) are formed after the quad
+//     loop; per quad the planes and gamma words go to L 16-byte vectors
+//     (one per plane, the quad's 4 nodes each), and the warp zeroes its
+//     quads' new state words.
+//   phase B (lane = task = one predictor function of one node):
+//     the parents' bit-sliced words are gathered (A6: one LDS per parent for
+//     all 32 chains), the function's truth table is evaluated on them as a
+//     multiplexer tree (entry masks at the leaves, one LOP3 per inner node:
+//     bit l of the result is table[idx of chain l]), masked by the
+//     function's selection plane and OR-ed into the node's new word (A7:
+//     the chains' selections are disjoint, so the OR over a node's tasks is
+//     f(s)); the task of function 0 also adds the perturbation term --
+//     VECTOR: chains with any gamma (M) take s XOR gamma;
+//     PER_NODE: chains with gamma_i take NOT s_i.
+//   statistics (A8-A10): as K1, on the committed words.
+//
+// Per node-update the work is one quarter of a Philox call, L-1 compare +
+// ballot pairs and ~1/32 of the task's gather and tree (SURVEY §8(d) demand
+// line "K1b") instead of K1's per-chain gather of FT padded
+// parents and per-chain descriptor reads.  Every output is bit-identical to
+// K1's (the same stream, thresholds, tables and statistics).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+
+#include "pbn_internal.h"
+#include "pbn_node.cuh"
+
+namespace pbn {
+namespace {
+
+__device__ __forceinline__ uint4 lds128_state(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v)
+{
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// table entry E as a word mask (all ones iff the entry is 1)
+template <int E>
+__device__ __forceinline__ uint32_t entry_mask(uint32_t t0, uint32_t t1)
+{
+    const uint32_t w = E < 32 ? t0 : t1;
+    return (uint32_t)((int32_t)(w << (31 - (E & 31))) >> 31);
+}
+
+// multiplexer tree: the sub-table of entries [B, B + 2^(C-K)) evaluated on
+// the parent words x[K..C-1] (x[0] = parents[0] = the index MSB, reading Q5):
+// x[K] = 0 selects the lower half, 1 the upper -- bit l of the result is the
+// entry at chain l's index
+template <int K, int C, int B>
+__device__ __forceinline__ uint32_t mux_tree(uint32_t t0, uint32_t t1, const uint32_t (&x)[C])
+{
+    if constexpr (K == C) {
+        return entry_mask<B>(t0, t1);
+    } else {
+        constexpr int H = 1 << (C - K - 1);
+        const uint32_t lo = mux_tree<K + 1, C, B>(t0, t1, x);
+        const uint32_t hi = mux_tree<K + 1, C, B + H>(t0, t1, x);
+        return (x[K] & hi) | (~x[K] & lo);
+    }
+}
+
+// one round of 32 tasks of class C (theta = C parents), lane = task; the
+// node's plane words are at pl + 16 m (m = 0..L-2: s_{m+1}; m = L-1: gamma)
+template <int C, int MODE, int L, uint32_t OB>
+__device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t sel, uint32_t M)
+{
+    constexpr uint32_t NB = 16u - OB;
+    uint32_t t0, t1 = 0, w0, w1, w2, w3 = 0;
+    if constexpr (C <= 5) {
+        const uint4 r = lds128_ro(ta);
+        t0 = r.x;
+        w0 = r.y;
+        w1 = r.z;
+        w2 = r.w;
+    } else {
+        const uint4 r = lds128_ro(ta);
+        const uint2 r2 = lds64_ro(ta + 16u);
+        t0 = r.x;
+        t1 = r.y;
+        w0 = r.z;
+        w1 = r.w;
+        w2 = r2.x;
+        w3 = r2.y;
+    }
+    const uint32_t pw[6] = {w0 >> 16, w1 & 0xFFFFu, w1 >> 16, w2 & 0xFFFFu, w2 >> 16, w3 & 0xFFFFu};
+    uint32_t x[C];
+#pragma unroll
+    for (int m = 0; m < C; ++m) x[m] = lds32_state(gbase + pw[m] + OB);
+    const uint32_t F = mux_tree<0, C, 0>(t0, t1, x);
+    const uint32_t i = (w0 & 0xFFFFu) >> 2, j = w0 & 3u;
+    const uint32_t pl = sel + 16u * (uint32_t)L * (i >> 2) + 4u * (i & 3u);
+    // selection plane of function j: s_j & ~s_{j+1} (s_0 = all chains, s_L = none)
+    const uint32_t s_lo = j == 0 ? FULL : lds32_state(pl + 16u * (j - 1u));
+    const uint32_t s_hi = j == (uint32_t)(L - 1) ? 0u : lds32_state(pl + 16u * j);
+    const uint32_t gam = lds32_state(pl + 16u * (uint32_t)(L - 1));
+    const uint32_t out = gbase + state_off(i);
+    const uint32_t old = lds32_state(out + OB);
+    const uint32_t first = j == 0 ? FULL : 0u;  // function 0 carries the perturbation term
+    uint32_t c;
+    if (MODE == 1) {  // PER_NODE: chains with gamma_i take NOT s_i
+        c = (F & s_lo & ~s_hi & ~gam) | (~old & gam & first);
+    } else {          // VECTOR: chains with any gamma take s XOR gamma
+        c = (F & s_lo & ~s_hi & ~M) | ((old ^ gam) & M & first);
+    }
+    if (c) red_or_shared(out + NB, c);
+}
+
+// MODE: 0 VECTOR, 1 PER_NODE; L = the model's largest ell (planes s_1..s_{L-1})
+template <int MODE, int L>
+__global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
+{
+    const TrajParams& P = B.T;
+    constexpr bool PER_NODE = MODE == 1;
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(8) uint64_t mbar;
+
+    const int tid = threadIdx.x;
+    const int wg = tid >> 5;
+    const int lane = tid & 31;
+    const int W = P.warps_per_group;
+    const int n = P.n;
+    const uint32_t gbase = smem_u32(smem);
+    const uint32_t sbase = gbase + 4u * (uint32_t)P.group_words;  // image base
+
+    // ---- A1: stage the image into shared memory (bulk async copy) ----
+    {
+        const uint32_t bar = smem_u32(&mbar);
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(P.image_smem_bytes)
+                         : "memory");
+            const uint32_t chunk = 32768;
+            for (uint32_t off = 0; off < P.image_smem_bytes; off += chunk) {
+                const uint32_t sz = min(chunk, P.image_smem_bytes - off);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sbase + off),
+                    "l"(P.image + off), "r"(sz), "r"(bar)
+                    : "memory");
+            }
+        }
+        __syncthreads();
+        asm volatile(
+            "{\n.reg .pred p;\nWAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+            "@!p bra WAIT_%=;\n}\n" ::"r"(bar)
+            : "memory");
+    }
+
+    const bool leader = lane == 0;
+    const uint32_t lead = leader ? FULL : 0u;
+    const uint32_t anyw = gbase + (uint32_t)B.any_off;
+    const uint32_t sel = gbase + (uint32_t)B.sel_off;
+    const uint32_t erec = sbase + B.erec_off;
+    const uint32_t rounds = sbase + B.rounds_off;
+    const int R = B.n_rounds;
+
+    const int NW = P.node_warps;
+    const int q0 = wg < NW ? (int)((int64_t)wg * P.nquads / NW) : P.nquads;
+    const int q1 = wg < NW ? (int)((int64_t)(wg + 1) * P.nquads / NW) : P.nquads;
+    const int nsw = P.state_words;
+    const int b0 = (int)((int64_t)wg * nsw / W), b1 = (int)((int64_t)(wg + 1) * nsw / W);
+    const int64_t total = P.burn_in + P.steps;
+    const uint32_t Tp = P.Tp;
+    const bool full_quads = (n & 3) == 0 || q1 < P.nquads;
+    __shared__ unsigned long long s_unit;
+
+    for (int64_t it = 0;; ++it) {
+        int64_t group, chunk, r_begin, r_end;
+        if (!P.persistent) {
+            if (it > 0) break;
+            group = blockIdx.x;
+            chunk = 0;
+            r_begin = 1;
+            r_end = total;
+        } else {
+            __syncthreads();
+            if (tid == 0) s_unit = atomicAdd(P.work_ctr, 1ull);
+            __syncthreads();
+            const unsigned long long u = __reduce_max_sync(FULL, (uint32_t)s_unit);
+            if (u >= (unsigned long long)P.total_units) break;
+            group = (int64_t)(u % (unsigned long long)P.n_groups);
+            chunk = (int64_t)(u / (unsigned long long)P.n_groups);
+            r_begin = chunk * P.chunk_steps + 1;
+            r_end = min(total, (chunk + 1) * P.chunk_steps);
+            if (chunk > 0 && tid == 0) {
+                for (;;) {
+                    unsigned int d;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(P.done + group) : "memory");
+                    if ((int64_t)d >= chunk) break;
+                    __nanosleep(256);
+                }
+            }
+        }
+        const bool first_chunk = chunk == 0;
+        const bool last_chunk = r_end >= total;
+        const uint32_t chain_local = (uint32_t)group * 32u + (uint32_t)lane;
+        const bool valid = (int64_t)chain_local < P.n_chains;
+        const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
+        const uint32_t vmask = __ballot_sync(FULL, valid);
+        uint32_t cur = 0;
+        auto scr = [&]() { return P.scratch + group * (int64_t)P.scratch_stride; };
+        const int prop = wg - P.stats_warp0;
+        const bool stats = prop >= 0 && prop < P.n_props;
+        auto orow = [&]() { return (int64_t)prop * P.n_chains + chain_local; };
+        ChainStats cs;
+
+        if (!first_chunk) {
+            __syncthreads();
+            for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr() + i));
+            if (stats) {
+                const uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
+                cs.c1 = __ldcg(st + 0);
+                cs.n01 = __ldcg(st + 1);
+                cs.n10 = __ldcg(st + 2);
+                cs.first = __ldcg(st + 3);
+                cs.prev = __ldcg(st + 4);
+                cs.bacc = __ldcg(st + 5);
+                cs.bitw = __ldcg(st + 6);
+                cs.bcount = __ldcg(st + 7);
+            }
+        } else if (P.init) {
+            // A2: s_0[i] = u(chain, 0, i) >> 31
+            for (int q = q0; q < q1; ++q) {
+                const uint4 r = philox4x32_10((uint32_t)q, chain, 0u, 0u, P.rk);
+                const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = 4 * q + k;
+                    if (i < n) {
+                        const uint32_t wv = __ballot_sync(FULL, (rr[k] >> 31) != 0u);
+                        if (leader) sts32(gbase + state_off(i), wv);
+                    }
+                }
+            }
+        } else {
+            for (int b = b0; b < b1; ++b) {
+                const uint32_t v = valid ? P.state[(int64_t)chain_local * nsw + b] : 0u;
+                for (int k = 0; k < 32; ++k) {
+                    const int i = 32 * b + k;
+                    if (i >= n) break;
+                    const uint32_t wv = __ballot_sync(FULL, (v >> k) & 1u);
+                    if (leader) sts32(gbase + state_off(i), wv);
+                }
+            }
+        }
+        __syncthreads();
+
+        auto step = [&](const int64_t r, auto ob_c) {
+            constexpr uint32_t OB = decltype(ob_c)::value;
+            constexpr uint32_t NB = 16u - OB;
+            const uint64_t t = (uint64_t)(P.step0 + r);
+            const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
+            uint32_t any = 0;
+            const PhiloxStep ps = philox_step(chain, t_lo, t_hi, P.rk);
+            const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;
+
+            // ---- phase A: planes of one quad (u = its four Philox words) ----
+            // quad q's record: L vectors of 16 bytes at sel + 16 L q -- the planes
+            // s_1..s_{L-1} of its 4 nodes, then their gamma words
+            auto planes = [&](const int q, const uint4 rw) {
+                const uint32_t ea = erec + 16u * (uint32_t)(L - 1) * (uint32_t)q;
+                const uint32_t pa = sel + 16u * (uint32_t)L * (uint32_t)q;
+#pragma unroll
+                for (int m = 0; m < L - 1; ++m) {
+                    const uint4 e = lds128_ro(ea + 16u * m);
+                    sts128_if(pa + 16u * m, __ballot_sync(FULL, rw.x > e.x), __ballot_sync(FULL, rw.y > e.y),
+                              __ballot_sync(FULL, rw.z > e.z), __ballot_sync(FULL, rw.w > e.w), lead);
+                }
+                sts128_if(pa + 16u * (L - 1), 0u, 0u, 0u, 0u, lead);                  // gamma (flagged quads: below)
+                sts128_if(gbase + 32u * (uint32_t)q + NB, 0u, 0u, 0u, 0u, lead);  // new words, OR-ed in phase B
+            };
+            auto gammas = [&](const int q, const uint4 rq) {
+                const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
+                const uint32_t g2 = __ballot_sync(FULL, rq.z < Tp), g3 = __ballot_sync(FULL, rq.w < Tp);
+                any |= g0 | g1 | g2 | g3;
+                sts128_if(sel + 16u * (uint32_t)L * (uint32_t)q + 16u * (L - 1), g0, g1, g2, g3, lead);
+            };
+            uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
+            for (int qc = q0; qc < qf; qc += 32) {
+                const int qe = min(qf, qc + 32);
+                uint32_t gpend = 0;  // flags of the chunk's quads, newest = bit 0
+                for (int q = qc; q < qe; ++q) {
+                    const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
+                    const uint32_t vq = __ballot_sync(FULL, min(min(rw.x, rw.y), min(rw.z, rw.w)) < Tp);
+                    planes(q, rw);
+                    gpend = gpend * 2u + min(vq, 1u);
+                    rw = rn;
+                }
+                // flagged quads: their gamma words (A4)
+                while (gpend) {
+                    const int jb = __ffs((int)gpend) - 1;
+                    gpend &= gpend - 1;
+                    const int q = qe - 1 - jb;
+                    gammas(q, philox_quad((uint32_t)q, ps, P.rk));
+                }
+            }
+            if (qf < q1) {  // ragged last quad: padding nodes draw no perturbation
+                const int q = qf;
+                const uint32_t nv = (uint32_t)(n - 4 * q);  // 1..3 real nodes
+                const uint4 rq = make_uint4(rw.x, nv > 1 ? rw.y : FULL, nv > 2 ? rw.z : FULL, FULL);
+                planes(q, rq);
+                gammas(q, rq);
+            }
+            if (!PER_NODE && leader) sts32(anyw + 4u * wg, any);
+            __syncthreads();
+
+            // ---- phase B: function tasks, 32 per round, rounds in snake order ----
+            uint32_t M = 0;
+            if (!PER_NODE) M = __reduce_or_sync(FULL, lane < W ? lds32(anyw + 4u * lane) : 0u) & vmask;
+            for (int m = 0; m * W < R; ++m) {
+                const int rr_i = (m & 1) ? (m + 1) * W - 1 - wg : m * W + wg;
+                if (rr_i >= R) continue;
+                const uint2 rr = lds64_ro(rounds + 8u * (uint32_t)rr_i);
+                const uint32_t ta = sbase + rr.x + (uint32_t)lane * (rr.y == 6u ? 32u : 16u);
+                switch (rr.y) {
+                    case 1: bs_round<1, MODE, L, OB>(ta, gbase, sel, M); break;
+                    case 2: bs_round<2, MODE, L, OB>(ta, gbase, sel, M); break;
+                    case 3: bs_round<3, MODE, L, OB>(ta, gbase, sel, M); break;
+                    case 4: bs_round<4, MODE, L, OB>(ta, gbase, sel, M); break;
+                    case 5: bs_round<5, MODE, L, OB>(ta, gbase, sel, M); break;
+                    default: bs_round<6, MODE, L, OB>(ta, gbase, sel, M); break;
+                }
+            }
+            __syncthreads();
+            if (stats && r > P.burn_in) {
+                const uint32_t b = ChainStats::indicator(P, prop, lane, [&](uint32_t i) { return gbase + state_off(i) + NB; });
+                cs.record(P, b, r - P.burn_in - 1, valid, orow());
+            }
+        };
+        for (int64_t r = r_begin; r <= r_end; r += 2) {
+            step(r, std::integral_constant<uint32_t, 0u>());
+            if (r + 1 <= r_end) step(r + 1, std::integral_constant<uint32_t, 16u>());
+        }
+        if (r_end >= r_begin && ((r_end - r_begin + 1) & 1)) cur = 16u;
+
+        if (!last_chunk) {
+            for (int i = tid; i < n; i += blockDim.x) __stcg(scr() + i, lds32(gbase + state_off(i) + cur));
+            if (stats) {
+                uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
+                __stcg(st + 0, cs.c1);
+                __stcg(st + 1, cs.n01);
+                __stcg(st + 2, cs.n10);
+                __stcg(st + 3, cs.first);
+                __stcg(st + 4, cs.prev);
+                __stcg(st + 5, cs.bacc);
+                __stcg(st + 6, cs.bitw);
+                __stcg(st + 7, cs.bcount);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.done + group), "r"((uint32_t)(chunk + 1))
+                             : "memory");
+            }
+            continue;
+        }
+        for (int b = b0; b < b1; ++b) {
+            uint32_t v = 0;
+            for (int k = 0; k < 32; ++k) {
+                const int i = 32 * b + k;
+                if (i >= n) break;
+                v |= ((lds32(gbase + state_off(i) + cur) >> lane) & 1u) << k;
+            }
+            if (valid) P.state[(int64_t)chain_local * nsw + b] = v;
+        }
+        if (stats) cs.finish(P, prop, valid, orow(), leader);
+    }
+}
+
+template <int MODE>
+const void* pick_L(int L)
+{
+    switch (L) {
+        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1>);
+        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2>);
+        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3>);
+        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4>);
+    }
+}
+
+}  // namespace
+
+const void* pick_bitslice_kernel(int mode, int L) { return mode == 1 ? pick_L<1>(L) : pick_L<0>(L); }
+
+}  // namespace pbn

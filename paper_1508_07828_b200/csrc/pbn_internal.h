@@ -192,6 +192,51 @@ size_t nodepar_smem_bytes(int n_words, int G, uint32_t max_sub_image);
 int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, void* stream);
 int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem_bytes, int* out);
 
+// Bit-sliced evaluation launch (pbn_bitslice.cu, K1b): the K1 group layout
+// (one 32-chain group per CTA, bit-sliced state words) with the node step
+// split in two phases per step:
+//   A  lane = chain: Philox words, and per node the selection planes
+//      s_m = ballot(u > E_m), m = 1..L-1 (and gamma = ballot(u < T_p) for the
+//      ~1 % of quads where some chain drew one), stored per quad as L
+//      16-byte vectors (s_1..s_{L-1}, gamma of its 4 nodes); each warp
+//      zeroes its quads' new words
+//   B  lane = (node, function) task: the function is evaluated for all 32
+//      chains at once on the parents' bit-sliced words (a multiplexer tree
+//      over its truth table), masked by its selection plane s_j & ~s_{j+1}
+//      and OR-ed into the node's new word (the chains' selections are
+//      disjoint, so the OR of all tasks of a node is the new word)
+// BITSLICE image (staged whole into shared memory, byte offsets from its start):
+//   erec   [nquads][L-1] uint4: E_{m+1} of the quad's 4 nodes (0xFFFFFFFF
+//          when m + 1 >= ell or the node is padding: the plane is 0)
+//   tasks  per class c = max(theta, 1) = 1..6, padded to whole rounds of 32
+//          (dummy tasks: table 0), stride 16 bytes (c <= 5) or 32 (c = 6):
+//            c <= 5: {t, (i << 2 | j) | p0 << 16, p1 | p2 << 16, p3 | p4 << 16}
+//            c = 6:  {t0, t1, (i << 2 | j) | p0 << 16, p1 | p2 << 16}
+//                    {p3 | p4 << 16, p5, 0, 0}
+//          t = the 2^c-entry table, entry e at bit e (t1: entries 32..63),
+//          idx = sum_m x(p_m) 2^(c-1-m) (parents[0] the MSB, reading Q5);
+//          i = node, j = function index within the node, p_m = state_off of
+//          parent m (u16 bytes; theta = 0 pads one ignored parent)
+//   rounds [n_rounds] uint2 {byte offset of the round's first task, c},
+//          most expensive class first (warps take them in snake order)
+constexpr int kBitsliceMaxTheta = 6;
+constexpr int kBitsliceMaxEll = 4;
+constexpr int kBitsliceMaxNodes = 8188;  // u16 state offsets and node ids << 2
+struct BitsliceParams {
+    TrajParams T;              // T.image = the bitslice image
+    uint32_t erec_off;         // image offsets
+    uint32_t rounds_off;
+    int32_t n_rounds;
+    int32_t sel_off;           // byte offset of the node plane records from the group state base
+    int32_t any_off;           // byte offset of the per-warp any words from the group state base
+};
+// group shared memory of the bitslice kernel (u32 words): 2 state buffers,
+// 32 any words, per quad the L plane vectors {s_1..s_{L-1}, gamma} of its 4 nodes
+inline int32_t bitslice_group_words(int32_t n_pad, int32_t L) { return 2 * n_pad + 32 + L * n_pad; }
+const void* pick_bitslice_kernel(int mode, int L);
+// K1's default warps per group for ceil(n/4) quads (pbn_traj.cu)
+int default_group_warps(int nquads);
+
 struct LaunchPlan {
     int warps_per_group;
     int node_warps;
@@ -220,6 +265,11 @@ int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan
 size_t traj_workspace_bytes(const TrajParams& P);
 int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, int64_t chunk_steps, void* workspace,
                 size_t workspace_bytes, void* stream);
+// The (group, step-chunk) unit schedule of launch_traj for any kernel whose
+// parameter struct embeds P (`kparams` is the kernel's single argument; the
+// persistent fields are filled in P, which must live inside *kparams).
+int launch_group_units(TrajParams& P, const void* fn, void* kparams, const LaunchPlan& plan, int device, int schedule,
+                       int64_t chunk_steps, void* workspace, size_t workspace_bytes, void* stream);
 
 struct RecountParams {
     const uint32_t* bits;

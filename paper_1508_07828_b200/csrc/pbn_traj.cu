@@ -96,6 +96,8 @@ int default_warps(int nquads)
 
 }  // namespace
 
+int default_group_warps(int nquads) { return default_warps(nquads); }
+
 int plan_traj_launch(const TrajParams& P, int device, int want_warps, LaunchPlan* plan, const char** why)
 {
     const int smem_optin = cached_device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -152,6 +154,12 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
     P.image_smem_bytes = plan.image_in_smem ? P.L.bytes : 0u;
     const int mode = P.per_node ? 1 : P.geometric ? 2 : 0;
     const void* fn = pick_kernel(plan.image_in_smem, mode, P.L.fast_theta, P.L.slow_nodes > 0);
+    return launch_group_units(P, fn, &P, plan, device, schedule, chunk_steps, workspace, workspace_bytes, stream);
+}
+
+int launch_group_units(TrajParams& P, const void* fn, void* kparams, const LaunchPlan& plan, int device, int schedule,
+                       int64_t chunk_steps, void* workspace, size_t workspace_bytes, void* stream)
+{
     cudaError_t e = ensure_func_smem(fn, plan.smem_bytes, false);
     if (e != cudaSuccess) return (int)e;
     cudaStream_t s = (cudaStream_t)stream;
@@ -204,7 +212,7 @@ int launch_traj(TrajParams P, const LaunchPlan& plan, int device, int schedule, 
         if (e != cudaSuccess) return (int)e;
         ctas = (int)std::min<int64_t>(resident, P.total_units);
     }
-    void* args[] = {&P};
+    void* args[] = {kparams};
     e = cudaLaunchKernel(fn, dim3(ctas), dim3(plan.threads), args, plan.smem_bytes, s);
     if (owned) {
         const cudaError_t e2 = cudaFreeAsync(ws, s);
