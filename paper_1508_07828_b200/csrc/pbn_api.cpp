@@ -505,7 +505,7 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
                 T[e >> 5] |= table_bit(d, f, e >> (c - theta)) << (e & 31u);
             uint32_t p[6] = {0, 0, 0, 0, 0, 0};
             for (int32_t m = 0; m < c; ++m)
-                p[m] = pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u);
+                p[m] = pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u, pbn::kBitsliceQs);
             const uint32_t ij = ((uint32_t)i << 2) | (uint32_t)j;
             if (c <= 5) {
                 w[0] = T[0];
@@ -804,8 +804,9 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.erec_off = m->bs_erec_off;
     Bp.rounds_off = m->bs_rounds_off;
     Bp.n_rounds = m->bs_rounds;
-    Bp.any_off = 8 * P.n_pad;
-    Bp.sel_off = 8 * P.n_pad + 128;
+    Bp.any_off = 12 * P.n_pad;
+    Bp.sel_off = 12 * P.n_pad + 272;
+    Bp.sel_bytes = 4 * m->bs_L * P.n_pad;
     int W = a->warps_per_group > 0 ? a->warps_per_group : pbn::default_group_warps(P.nquads);
     W = std::max(W, P.n_props);
     if (W > pbn::kMaxWarpsPerCta || W > std::max(P.nquads, P.n_props)) return PBN_E_USAGE;

@@ -4,9 +4,9 @@
 // The same hot path as K1 (§2.2) on
 // the same group layout -- one 32-chain group per CTA, its state bit-sliced
 // in shared memory (word i = node i of the 32 chains, bit l = chain of lane
-// l, two interleaved buffers, pbn_internal.h) -- but the node step is split
-// in two phases so that the truth-table work is done once per 32 chains
-// instead of once per chain:
+// l; here THREE interleaved buffers, pbn_internal.h) -- but the node step is
+// split in two phases so that the truth-table work is done once per 32
+// chains instead of once per chain:
 //
 //   phase A (lane = chain; every warp its quads of nodes, as K1):
 //     one Philox4x32-10 call per quad (A3, reading Q2); per node the
@@ -14,9 +14,8 @@
 //     function j = #{m : u_l > E_m}, so bit l of s_j & ~s_{j+1} is set iff
 //     chain l picks j); one vote per quad flags the ~1 % of quads where some
 //     chain drew u < T_p, whose gamma words (A4) are formed after the quad
-//     loop; per quad the planes and gamma words go to L 16-byte vectors
-//     (one per plane, the quad's 4 nodes each), and the warp zeroes its
-//     quads' new state words.
+//     loop; per quad the planes and gamma words go to L 16-byte vectors, and
+//     the warp zeroes its quads' words of the step's state buffer.
 //   phase B (lane = task = one predictor function of one node):
 //     the parents' bit-sliced words are gathered (A6: one LDS per parent for
 //     all 32 chains), the function's truth table is evaluated on them as a
@@ -29,11 +28,18 @@
 //     PER_NODE: chains with gamma_i take NOT s_i.
 //   statistics (A8-A10): as K1, on the committed words.
 //
+// Phase A reads no state, so phase A of step t+1 shares an interval with
+// phase B of step t (even warps A first, odd warps B first, so the pipes see
+// both instruction mixes at once): one CTA barrier per step; the planes and
+// any words are double-buffered by step parity and the state triple-buffered
+// (B(t) reads S_{t-1}, ORs into S_t; A(t+1) zeroes S_{t+1}'s buffer; the
+// statistics warp reads S_t in the next interval).
+//
 // Per node-update the work is one quarter of a Philox call, L-1 compare +
-// ballot pairs and ~1/32 of the task's gather and tree (SURVEY §8(d) demand
-// line "K1b") instead of K1's per-chain gather of FT padded
-// parents and per-chain descriptor reads.  Every output is bit-identical to
-// K1's (the same stream, thresholds, tables and statistics).
+// ballot pairs and ~1/32 of the task's gather and tree instead
+// of K1's per-chain gather of FT padded parents and per-chain descriptor
+// reads.  Every output is bit-identical to K1's (the same stream,
+// thresholds, tables and statistics).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,18 +51,6 @@
 
 namespace pbn {
 namespace {
-
-__device__ __forceinline__ uint4 lds128_state(uint32_t a)
-{
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-
-__device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v)
-{
-    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 
 // table entry E as a word mask (all ones iff the entry is 1)
 template <int E>
@@ -83,12 +77,13 @@ __device__ __forceinline__ uint32_t mux_tree(uint32_t t0, uint32_t t1, const uin
     }
 }
 
-// one round of 32 tasks of class C (theta = C parents), lane = task; the
-// node's plane words are at pl + 16 m (m = 0..L-2: s_{m+1}; m = L-1: gamma)
-template <int C, int MODE, int L, uint32_t OB>
-__device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t sel, uint32_t M)
+// one round of 32 tasks of class C (theta = C parents), lane = task.  The
+// node's plane words are at pl + 16 m (m = 0..L-2: s_{m+1}; m = L-1:
+// gamma); `cw` holds the constant words FULL (cw) and ZERO (cw + 4) that
+// stand in for s_0 and s_L, so every load is unconditional.
+template <int C, int MODE, int L, uint32_t OB, uint32_t NB>
+__device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t sel, uint32_t cw, uint32_t M)
 {
-    constexpr uint32_t NB = 16u - OB;
     uint32_t t0, t1 = 0, w0, w1, w2, w3 = 0;
     if constexpr (C <= 5) {
         const uint4 r = lds128_ro(ta);
@@ -114,10 +109,10 @@ __device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t s
     const uint32_t i = (w0 & 0xFFFFu) >> 2, j = w0 & 3u;
     const uint32_t pl = sel + 16u * (uint32_t)L * (i >> 2) + 4u * (i & 3u);
     // selection plane of function j: s_j & ~s_{j+1} (s_0 = all chains, s_L = none)
-    const uint32_t s_lo = j == 0 ? FULL : lds32_state(pl + 16u * (j - 1u));
-    const uint32_t s_hi = j == (uint32_t)(L - 1) ? 0u : lds32_state(pl + 16u * j);
+    const uint32_t s_lo = lds32_state(j == 0 ? cw : pl + 16u * (j - 1u));
+    const uint32_t s_hi = lds32_state(j == (uint32_t)(L - 1) ? cw + 4u : pl + 16u * j);
     const uint32_t gam = lds32_state(pl + 16u * (uint32_t)(L - 1));
-    const uint32_t out = gbase + state_off(i);
+    const uint32_t out = gbase + state_off(i, kBitsliceQs);
     const uint32_t old = lds32_state(out + OB);
     const uint32_t first = j == 0 ? FULL : 0u;  // function 0 carries the perturbation term
     uint32_t c;
@@ -126,7 +121,9 @@ __device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t s
     } else {          // VECTOR: chains with any gamma take s XOR gamma
         c = (F & s_lo & ~s_hi & ~M) | ((old ^ gam) & M & first);
     }
-    if (c) red_or_shared(out + NB, c);
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(out + NB),
+                 "r"(c)
+                 : "memory");
 }
 
 // MODE: 0 VECTOR, 1 PER_NODE; L = the model's largest ell (planes s_1..s_{L-1})
@@ -135,6 +132,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
 {
     const TrajParams& P = B.T;
     constexpr bool PER_NODE = MODE == 1;
+    constexpr uint32_t QS = kBitsliceQs;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
 
@@ -174,11 +172,16 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
 
     const bool leader = lane == 0;
     const uint32_t lead = leader ? FULL : 0u;
-    const uint32_t anyw = gbase + (uint32_t)B.any_off;
-    const uint32_t sel = gbase + (uint32_t)B.sel_off;
+    const uint32_t anyw0 = gbase + (uint32_t)B.any_off;  // any[2][32]
+    const uint32_t cw = anyw0 + 256u;                    // constant words FULL, ZERO
+    const uint32_t sel0 = gbase + (uint32_t)B.sel_off;   // planes[2]
     const uint32_t erec = sbase + B.erec_off;
     const uint32_t rounds = sbase + B.rounds_off;
     const int R = B.n_rounds;
+    if (tid == 0) {
+        sts32(cw, FULL);
+        sts32(cw + 4u, 0u);
+    }
 
     const int NW = P.node_warps;
     const int q0 = wg < NW ? (int)((int64_t)wg * P.nquads / NW) : P.nquads;
@@ -188,6 +191,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
     const int64_t total = P.burn_in + P.steps;
     const uint32_t Tp = P.Tp;
     const bool full_quads = (n & 3) == 0 || q1 < P.nquads;
+    const bool a_first = (wg & 1) == 0;  // even warps: A(t+1) then B(t); odd: B(t) then A(t+1)
     __shared__ unsigned long long s_unit;
 
     for (int64_t it = 0;; ++it) {
@@ -223,16 +227,16 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
         const bool valid = (int64_t)chain_local < P.n_chains;
         const uint32_t chain = (uint32_t)(P.chain_base + chain_local);
         const uint32_t vmask = __ballot_sync(FULL, valid);
-        uint32_t cur = 0;
         auto scr = [&]() { return P.scratch + group * (int64_t)P.scratch_stride; };
         const int prop = wg - P.stats_warp0;
         const bool stats = prop >= 0 && prop < P.n_props;
         auto orow = [&]() { return (int64_t)prop * P.n_chains + chain_local; };
         ChainStats cs;
 
+        // S_0 of the unit into state buffer 0
         if (!first_chunk) {
             __syncthreads();
-            for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i), __ldcg(scr() + i));
+            for (int i = tid; i < n; i += blockDim.x) sts32(gbase + state_off(i, QS), __ldcg(scr() + i));
             if (stats) {
                 const uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
                 cs.c1 = __ldcg(st + 0);
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
                     const int i = 4 * q + k;
                     if (i < n) {
                         const uint32_t wv = __ballot_sync(FULL, (rr[k] >> 31) != 0u);
-                        if (leader) sts32(gbase + state_off(i), wv);
+                        if (leader) sts32(gbase + state_off(i, QS), wv);
                     }
                 }
             }
@@ -265,35 +269,41 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
                     const int i = 32 * b + k;
                     if (i >= n) break;
                     const uint32_t wv = __ballot_sync(FULL, (v >> k) & 1u);
-                    if (leader) sts32(gbase + state_off(i), wv);
+                    if (leader) sts32(gbase + state_off(i, QS), wv);
                 }
             }
         }
-        __syncthreads();
 
-        auto step = [&](const int64_t r, auto ob_c) {
-            constexpr uint32_t OB = decltype(ob_c)::value;
-            constexpr uint32_t NB = 16u - OB;
-            const uint64_t t = (uint64_t)(P.step0 + r);
+        // unit step k = 1..K is step r = r_begin - 1 + k; S_k in buffer k % 3
+        const int64_t K = r_end - r_begin + 1;
+
+        // ---- phase A of unit step k: planes -> planes[k & 1], zero S_k's buffer ZB ----
+        auto phaseA = [&](const int64_t k, auto zb_c) {
+            constexpr uint32_t ZB = decltype(zb_c)::value;
+            const uint64_t t = (uint64_t)(P.step0 + r_begin - 1 + k);
             const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
+            const uint32_t sel = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes;
             uint32_t any = 0;
             const PhiloxStep ps = philox_step(chain, t_lo, t_hi, P.rk);
             const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;
-
-            // ---- phase A: planes of one quad (u = its four Philox words) ----
             // quad q's record: L vectors of 16 bytes at sel + 16 L q -- the planes
             // s_1..s_{L-1} of its 4 nodes, then their gamma words
-            auto planes = [&](const int q, const uint4 rw) {
+            auto thresholds = [&](const int q, uint4 (&e)[3]) {
                 const uint32_t ea = erec + 16u * (uint32_t)(L - 1) * (uint32_t)q;
-                const uint32_t pa = sel + 16u * (uint32_t)L * (uint32_t)q;
 #pragma unroll
-                for (int m = 0; m < L - 1; ++m) {
-                    const uint4 e = lds128_ro(ea + 16u * m);
-                    sts128_if(pa + 16u * m, __ballot_sync(FULL, rw.x > e.x), __ballot_sync(FULL, rw.y > e.y),
-                              __ballot_sync(FULL, rw.z > e.z), __ballot_sync(FULL, rw.w > e.w), lead);
-                }
-                sts128_if(pa + 16u * (L - 1), 0u, 0u, 0u, 0u, lead);                  // gamma (flagged quads: below)
-                sts128_if(gbase + 32u * (uint32_t)q + NB, 0u, 0u, 0u, 0u, lead);  // new words, OR-ed in phase B
+                for (int m = 0; m < L - 1; ++m) e[m] = lds128_ro(ea + 16u * m);
+            };
+            auto planes = [&](const int q, const uint4 rw, const uint4 (&e)[3]) {
+                const uint32_t pa = sel + 16u * (uint32_t)L * (uint32_t)q;
+                uint4 s[3];
+#pragma unroll
+                for (int m = 0; m < L - 1; ++m)
+                    s[m] = make_uint4(__ballot_sync(FULL, rw.x > e[m].x), __ballot_sync(FULL, rw.y > e[m].y),
+                                      __ballot_sync(FULL, rw.z > e[m].z), __ballot_sync(FULL, rw.w > e[m].w));
+#pragma unroll
+                for (int m = 0; m < L - 1; ++m) sts128_if(pa + 16u * m, s[m].x, s[m].y, s[m].z, s[m].w, lead);
+                sts128_if(pa + 16u * (L - 1), 0u, 0u, 0u, 0u, lead);              // gamma (flagged quads: below)
+                sts128_if(gbase + QS * (uint32_t)q + ZB, 0u, 0u, 0u, 0u, lead);  // S_k's words, OR-ed in phase B
             };
             auto gammas = [&](const int q, const uint4 rq) {
                 const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
@@ -302,14 +312,20 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
                 sts128_if(sel + 16u * (uint32_t)L * (uint32_t)q + 16u * (L - 1), g0, g1, g2, g3, lead);
             };
             uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
+            uint4 e[3];
             for (int qc = q0; qc < qf; qc += 32) {
                 const int qe = min(qf, qc + 32);
                 uint32_t gpend = 0;  // flags of the chunk's quads, newest = bit 0
                 for (int q = qc; q < qe; ++q) {
-                    const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
+                    // the flag vote first: the quad's thresholds, the next
+                    // quad's Philox call and the plane ballots follow it in
+                    // one basic block, so the scheduler overlaps the loads'
+                    // latency and the Philox chain with the ballots
                     const uint32_t vq = __ballot_sync(FULL, min(min(rw.x, rw.y), min(rw.z, rw.w)) < Tp);
-                    planes(q, rw);
-                    gpend = gpend * 2u + min(vq, 1u);
+                    thresholds(q, e);
+                    const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
+                    planes(q, rw, e);
+                    asm("{\n\t.reg .u32 f;\n\tmin.u32 f, %1, 1;\n\tmad.lo.u32 %0, %0, 2, f;\n\t}" : "+r"(gpend) : "r"(vq));
                     rw = rn;
                 }
                 // flagged quads: their gamma words (A4)
@@ -324,43 +340,75 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
                 const int q = qf;
                 const uint32_t nv = (uint32_t)(n - 4 * q);  // 1..3 real nodes
                 const uint4 rq = make_uint4(rw.x, nv > 1 ? rw.y : FULL, nv > 2 ? rw.z : FULL, FULL);
-                planes(q, rq);
+                thresholds(q, e);
+                planes(q, rq, e);
                 gammas(q, rq);
             }
-            if (!PER_NODE && leader) sts32(anyw + 4u * wg, any);
-            __syncthreads();
+            if (!PER_NODE && leader) sts32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * wg, any);
+        };
 
-            // ---- phase B: function tasks, 32 per round, rounds in snake order ----
+        // ---- phase B of unit step k: S_k (buffer NB) from S_{k-1} (OB) and planes[k & 1] ----
+        auto phaseB = [&](const int64_t k, auto ob_c, auto nb_c) {
+            constexpr uint32_t OB = decltype(ob_c)::value;
+            constexpr uint32_t NB = decltype(nb_c)::value;
+            const uint32_t sel = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes;
             uint32_t M = 0;
-            if (!PER_NODE) M = __reduce_or_sync(FULL, lane < W ? lds32(anyw + 4u * lane) : 0u) & vmask;
+            if (!PER_NODE)
+                M = __reduce_or_sync(FULL, lane < W ? lds32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * lane) : 0u) & vmask;
             for (int m = 0; m * W < R; ++m) {
                 const int rr_i = (m & 1) ? (m + 1) * W - 1 - wg : m * W + wg;
                 if (rr_i >= R) continue;
                 const uint2 rr = lds64_ro(rounds + 8u * (uint32_t)rr_i);
                 const uint32_t ta = sbase + rr.x + (uint32_t)lane * (rr.y == 6u ? 32u : 16u);
                 switch (rr.y) {
-                    case 1: bs_round<1, MODE, L, OB>(ta, gbase, sel, M); break;
-                    case 2: bs_round<2, MODE, L, OB>(ta, gbase, sel, M); break;
-                    case 3: bs_round<3, MODE, L, OB>(ta, gbase, sel, M); break;
-                    case 4: bs_round<4, MODE, L, OB>(ta, gbase, sel, M); break;
-                    case 5: bs_round<5, MODE, L, OB>(ta, gbase, sel, M); break;
-                    default: bs_round<6, MODE, L, OB>(ta, gbase, sel, M); break;
+                    case 1: bs_round<1, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
+                    case 2: bs_round<2, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
+                    case 3: bs_round<3, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
+                    case 4: bs_round<4, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
+                    case 5: bs_round<5, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
+                    default: bs_round<6, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
                 }
             }
-            __syncthreads();
+        };
+
+        // statistics of unit step k (S_k in buffer BUF), statistics warps
+        auto record = [&](const int64_t k, const uint32_t buf) {
+            const int64_t r = r_begin - 1 + k;
             if (stats && r > P.burn_in) {
-                const uint32_t b = ChainStats::indicator(P, prop, lane, [&](uint32_t i) { return gbase + state_off(i) + NB; });
+                const uint32_t b = ChainStats::indicator(
+                    P, prop, lane, [&](uint32_t i) { return gbase + state_off(i, QS) + buf; });
                 cs.record(P, b, r - P.burn_in - 1, valid, orow());
             }
         };
-        for (int64_t r = r_begin; r <= r_end; r += 2) {
-            step(r, std::integral_constant<uint32_t, 0u>());
-            if (r + 1 <= r_end) step(r + 1, std::integral_constant<uint32_t, 16u>());
+
+        // one interval: statistics of k-1, phase B of k and phase A of k+1
+        auto interval = [&](const int64_t k, auto ob_c, auto nb_c, auto zb_c) {
+            if (k > 1) record(k - 1, decltype(ob_c)::value);
+            if (a_first) {
+                if (k < K) phaseA(k + 1, zb_c);
+                phaseB(k, ob_c, nb_c);
+            } else {
+                phaseB(k, ob_c, nb_c);
+                if (k < K) phaseA(k + 1, zb_c);
+            }
+            __syncthreads();
+        };
+        using C0 = std::integral_constant<uint32_t, 0u>;
+        using C1 = std::integral_constant<uint32_t, 16u>;
+        using C2 = std::integral_constant<uint32_t, 32u>;
+        if (K >= 1) phaseA(1, C1());
+        __syncthreads();
+        for (int64_t k = 1; k <= K; k += 3) {
+            interval(k, C0(), C1(), C2());
+            if (k + 1 <= K) interval(k + 1, C1(), C2(), C0());
+            if (k + 2 <= K) interval(k + 2, C2(), C0(), C1());
         }
-        if (r_end >= r_begin && ((r_end - r_begin + 1) & 1)) cur = 16u;
+        const uint32_t cur = 16u * (uint32_t)(K % 3);  // S_K's buffer
+        if (K >= 1) record(K, cur);
 
         if (!last_chunk) {
-            for (int i = tid; i < n; i += blockDim.x) __stcg(scr() + i, lds32(gbase + state_off(i) + cur));
+            __syncthreads();
+            for (int i = tid; i < n; i += blockDim.x) __stcg(scr() + i, lds32(gbase + state_off(i, QS) + cur));
             if (stats) {
                 uint32_t* st = scr() + P.n_pad + 8 * 32 * prop + 8 * lane;
                 __stcg(st + 0, cs.c1);
@@ -385,7 +433,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
             for (int k = 0; k < 32; ++k) {
                 const int i = 32 * b + k;
                 if (i >= n) break;
-                v |= ((lds32(gbase + state_off(i) + cur) >> lane) & 1u) << k;
+                v |= ((lds32(gbase + state_off(i, QS) + cur) >> lane) & 1u) << k;
             }
             if (valid) P.state[(int64_t)chain_local * nsw + b] = v;
         }

@@ -192,19 +192,22 @@ size_t nodepar_smem_bytes(int n_words, int G, uint32_t max_sub_image);
 int launch_traj_nodepar(const NodeParParams& C, int threads, size_t smem_bytes, void* stream);
 int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem_bytes, int* out);
 
-// Bit-sliced evaluation launch (pbn_bitslice.cu, K1b): the K1 group layout
-// (one 32-chain group per CTA, bit-sliced state words) with the node step
-// split in two phases per step:
+// Bit-sliced evaluation launch (pbn_bitslice.cu, K1b): one 32-chain group
+// per CTA with K1's bit-sliced state words (THREE interleaved buffers, quads
+// 48 bytes apart: state_off(i, 48) + 16 b), the node step split in two phases:
 //   A  lane = chain: Philox words, and per node the selection planes
 //      s_m = ballot(u > E_m), m = 1..L-1 (and gamma = ballot(u < T_p) for the
 //      ~1 % of quads where some chain drew one), stored per quad as L
 //      16-byte vectors (s_1..s_{L-1}, gamma of its 4 nodes); each warp
-//      zeroes its quads' new words
+//      zeroes its quads' words of the step's state buffer
 //   B  lane = (node, function) task: the function is evaluated for all 32
 //      chains at once on the parents' bit-sliced words (a multiplexer tree
 //      over its truth table), masked by its selection plane s_j & ~s_{j+1}
 //      and OR-ed into the node's new word (the chains' selections are
 //      disjoint, so the OR of all tasks of a node is the new word)
+// Phase A needs no state, so A of step t+1 runs in the same interval as B of
+// step t (planes and any words double-buffered by step parity, state
+// triple-buffered): one barrier per step.
 // BITSLICE image (staged whole into shared memory, byte offsets from its start):
 //   erec   [nquads][L-1] uint4: E_{m+1} of the quad's 4 nodes (0xFFFFFFFF
 //          when m + 1 >= ell or the node is padding: the plane is 0)
@@ -215,24 +218,26 @@ int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem
 //                    {p3 | p4 << 16, p5, 0, 0}
 //          t = the 2^c-entry table, entry e at bit e (t1: entries 32..63),
 //          idx = sum_m x(p_m) 2^(c-1-m) (parents[0] the MSB, reading Q5);
-//          i = node, j = function index within the node, p_m = state_off of
-//          parent m (u16 bytes; theta = 0 pads one ignored parent)
+//          i = node, j = function index within the node, p_m =
+//          state_off(parent m, 48) (u16 bytes; theta = 0 pads one ignored parent)
 //   rounds [n_rounds] uint2 {byte offset of the round's first task, c},
 //          most expensive class first (warps take them in snake order)
 constexpr int kBitsliceMaxTheta = 6;
 constexpr int kBitsliceMaxEll = 4;
-constexpr int kBitsliceMaxNodes = 8188;  // u16 state offsets and node ids << 2
+constexpr int kBitsliceMaxNodes = 5460;  // u16 state offsets 48 (i >> 2) + 4 (i & 3) and node ids << 2
+constexpr uint32_t kBitsliceQs = 48;     // bytes between quads: three interleaved state buffers
 struct BitsliceParams {
     TrajParams T;              // T.image = the bitslice image
     uint32_t erec_off;         // image offsets
     uint32_t rounds_off;
     int32_t n_rounds;
-    int32_t sel_off;           // byte offset of the node plane records from the group state base
-    int32_t any_off;           // byte offset of the per-warp any words from the group state base
+    int32_t sel_off;           // from the group state base: planes[2][nquads][L] uint4
+    int32_t sel_bytes;         // bytes of one plane buffer (16 L nquads)
+    int32_t any_off;           // from the group state base: any[2][32] words, then a FULL and a ZERO word
 };
-// group shared memory of the bitslice kernel (u32 words): 2 state buffers,
-// 32 any words, per quad the L plane vectors {s_1..s_{L-1}, gamma} of its 4 nodes
-inline int32_t bitslice_group_words(int32_t n_pad, int32_t L) { return 2 * n_pad + 32 + L * n_pad; }
+// group shared memory of the bitslice kernel (u32 words): 3 state buffers,
+// 2 x 32 any words + 4 constant words, 2 plane buffers of 4 L words per quad
+inline int32_t bitslice_group_words(int32_t n_pad, int32_t L) { return 3 * n_pad + 68 + 2 * L * n_pad; }
 const void* pick_bitslice_kernel(int mode, int L);
 // K1's default warps per group for ceil(n/4) quads (pbn_traj.cu)
 int default_group_warps(int nquads);
