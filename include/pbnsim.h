@@ -427,6 +427,13 @@ pbn_status pbn_run_multi(pbn_model model, const pbn_run_args* args, const pbn_pr
 /* Version string of the build, e.g. "libpbnsim 0.1 sm_100a". */
 const char* pbn_version(void);
 
+/* Name of the trajectory kernel the calling thread's most recent successful
+ * pbn_simulate launched: "K1b" (bit-sliced evaluation), "K1" (chain lanes,
+ * image in shared memory), "K1-global" (image through L1/L2), "K1c"
+ * (cluster), "K1n" (lanes over nodes); "" before the first launch.  A static
+ * string; thread-local state, no device call. */
+const char* pbn_last_kernel(void);
+
 #ifdef __cplusplus
 }
 #endif

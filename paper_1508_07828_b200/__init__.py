@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     pbn_run,
     pbn_run_multi,
     pbn_version,
+    pbn_last_kernel,
     alloc_outputs,
     PbnError,
 )

@@ -145,6 +145,7 @@ SIGNATURES = {
     "pbn_run_sharded": (C.c_int, [C.c_void_p, C.POINTER(pbn_run_args), C.c_int64, C.c_int64, C.c_void_p,
                                   C.c_void_p, C.POINTER(pbn_run_result), C.c_void_p, C.c_char_p, C.c_size_t]),
     "pbn_version": (C.c_char_p, []),
+    "pbn_last_kernel": (C.c_char_p, []),
 }
 
 # int (*)(uint64_t* values, int32_t count, void* ctx): in-place sum over shards

@@ -16,7 +16,8 @@ from ._lib import PbnError, check, lib
 __all__ = ["Model", "SimOutputs", "pbn_load", "pbn_validate", "pbn_simulate", "pbn_simulate_workspace_size",
            "pbn_recount",
            "pbn_gelman_rubin", "pbn_two_state", "pbn_inv_norm_cdf", "pbn_t_quantile",
-           "pbn_skart_ci_from_batches", "pbn_skart", "pbn_run", "pbn_version", "alloc_outputs", "PbnError"]
+           "pbn_skart_ci_from_batches", "pbn_skart", "pbn_run", "pbn_version", "pbn_last_kernel", "alloc_outputs",
+           "PbnError"]
 
 
 def _desc(m, per_node: bool, geometric: bool = False):
@@ -51,6 +52,11 @@ def _desc(m, per_node: bool, geometric: bool = False):
 
 def pbn_version() -> str:
     return lib().pbn_version().decode()
+
+
+def pbn_last_kernel() -> str:
+    """Kernel of this thread's last successful pbn_simulate ("K1b", "K1", "K1-global", "K1c", "K1n")."""
+    return lib().pbn_last_kernel().decode()
 
 
 def pbn_validate(model, per_node: bool = False) -> tuple[int, str]:

@@ -126,6 +126,9 @@ void set_err(char* err, size_t errlen, const char* fmt, ...)
 
 constexpr uint64_t kTwo32 = 1ull << 32;
 
+// pbn_last_kernel(): the kernel of this thread's last successful launch
+thread_local const char* g_last_kernel = "";
+
 uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 // ---------------------------------------------------------------------
@@ -557,6 +560,8 @@ extern "C" {
 
 const char* pbn_version(void) { return "libpbnsim 0.1 sm_100a"; }
 
+const char* pbn_last_kernel(void) { return g_last_kernel; }
+
 pbn_status pbn_validate(const pbn_model_desc* desc, char* err, size_t errlen)
 {
     return validate(desc, err, errlen);
@@ -807,7 +812,8 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.any_off = 12 * P.n_pad;
     Bp.sel_off = 12 * P.n_pad + 272;
     Bp.sel_bytes = 4 * m->bs_L * P.n_pad;
-    int W = a->warps_per_group > 0 ? a->warps_per_group : pbn::default_group_warps(P.nquads);
+    // 28 warps (the 72-register budget): C4 6.40e11 vs 6.30e11 node-updates/s at 20
+    int W = a->warps_per_group > 0 ? a->warps_per_group : std::min(pbn::kMaxWarpsPerCta, std::max(P.nquads, 1));
     W = std::max(W, P.n_props);
     if (W > pbn::kMaxWarpsPerCta || W > std::max(P.nquads, P.n_props)) return PBN_E_USAGE;
     pbn::LaunchPlan plan;
@@ -827,6 +833,7 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     const int rc = pbn::launch_group_units(Bp.T, fn, &Bp, plan, m->device, a->schedule, a->chunk_steps, a->workspace,
                                            (size_t)a->workspace_bytes, stream);
     if (rc == -2) return PBN_E_USAGE;
+    if (rc == 0) g_last_kernel = "K1b";
     return rc == 0 ? PBN_OK : PBN_E_CUDA;
 }
 
@@ -852,6 +859,15 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     if (a->layout == PBN_LAYOUT_BITSLICE) {
         if (a->cluster_size > 1 || a->chains_per_cluster != 0) return PBN_E_USAGE;
         return simulate_bitslice(m, P, a, stream, smem_optin);
+    }
+    // auto: the bit-sliced kernel wherever the one-CTA-per-group kernel would
+    // run (enough groups to fill the GPU) and the model has a bitslice image
+    // that fits (C3 4.15e11 -> 5.9e11, C4 5.32e11 -> 6.4e11 node-updates/s);
+    // cluster_size = 1 keeps asking for K1 itself
+    if (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 && m->d_bs && 2 * groups > sms &&
+        (size_t)pbn::bitslice_group_words(P.n_pad, m->bs_L) * 4 + m->bs_bytes <= limit) {
+        const char* nb = std::getenv("PBN_NO_BITSLICE");  // A/B knob: auto without K1b
+        if (!(nb && nb[0] == '1')) return simulate_bitslice(m, P, a, stream, smem_optin);
     }
     // ---- lanes over nodes (K1n): G chains per cluster of K CTAs ----
     const int32_t nw = (P.n + 31) / 32;
@@ -948,6 +964,7 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
         C.share = (int)(C.G * ow > threads / 32);
         const size_t smem = pbn::nodepar_smem_bytes(nw, C.G, np_use->max_bytes);
         const int rc = pbn::launch_traj_nodepar(C, threads, smem, stream);
+        if (rc == 0) g_last_kernel = "K1n";
         return rc == 0 ? PBN_OK : PBN_E_CUDA;
     }
     auto fits = [&](const ClusterImages& ci) { return pbn::cluster_smem_bytes(P, ci.max_bytes) <= limit; };
@@ -1003,6 +1020,7 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
             if (a->cluster_size >= 2) return PBN_E_USAGE;
         } else {
             const int rc = pbn::launch_traj_cluster(C, W, smem, stream);
+            if (rc == 0) g_last_kernel = "K1c";
             return rc == 0 ? PBN_OK : PBN_E_CUDA;
         }
     }
@@ -1016,6 +1034,7 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     rc = pbn::launch_traj(P, plan, m->device, a->schedule, a->chunk_steps, a->workspace, (size_t)a->workspace_bytes,
                           stream);
     if (rc == -2) return PBN_E_USAGE;
+    if (rc == 0) g_last_kernel = plan.image_in_smem ? "K1" : "K1-global";
     return rc == 0 ? PBN_OK : PBN_E_CUDA;
 }
 

@@ -148,14 +148,16 @@ def test_multi_property(pbn):
 
 @pytest.mark.parametrize("key", ["C3", "C4"])
 def test_large_configs_sampled_chains(pbn, key):
-    """The full C3 / C4 launch through K1b (the bench shape); the oracle
+    """The full C3 / C4 launch (auto: K1b, the bench shape); the oracle
     recomputes 64 sampled chains at the full step count; invariants on every
     chain."""
     c = CONFIGS[key]
     model, pred = config_model(key), config_predicate(key)
     pm = pbn.pbn_load(model)
+    # auto layout: the kernel bench.py times on these configs
     g = gpu_run(pm, model, pred, n_chains=c.chains, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed,
-                batch=c.batch, layout=BS)
+                batch=c.batch)
+    assert pbn.pbn_last_kernel() == "K1b"
     ids = sample_chain_ids(c.chains, k=64, seed=c.sim_seed)
     st, I, ws = oracle_run(model, pred, ids, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch,
                            threads=os.cpu_count() or 8)

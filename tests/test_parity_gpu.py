@@ -78,8 +78,13 @@ def test_large_configs_sampled_chains(pbn, key, n_chains):
     n_chains = n_chains or c.chains
     steps, burn_in = c.steps, c.burn_in
     pm = load(pbn, model)
+    # C3 / C4: the chain-lanes kernel K1 (layout 1); auto runs the bit-sliced
+    # K1b there, compared at these shapes in tests/test_bitslice_gpu.py
+    layout = 1 if key in ("C3", "C4") else 0
     g = gpu_run(pm, model, pred, n_chains=n_chains, steps=steps, burn_in=burn_in, seed=c.sim_seed,
-                batch=c.batch)
+                batch=c.batch, layout=layout)
+    if layout == 1:
+        assert pbn.pbn_last_kernel() == "K1"
     ids = sample_chain_ids(n_chains, k=64, seed=c.sim_seed)
     st, I, ws = oracle_run(model, pred, ids, steps=steps, burn_in=burn_in, seed=c.sim_seed,
                            batch=c.batch, threads=os.cpu_count() or 8)
