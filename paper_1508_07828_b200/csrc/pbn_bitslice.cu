@@ -52,6 +52,15 @@
 namespace pbn {
 namespace {
 
+// 16-byte shared load ordered with the barriers (the per-quad Philox table
+// is refilled when t_hi changes)
+__device__ __forceinline__ uint4 lds128_state(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
 // table entry E as a word mask (all ones iff the entry is 1)
 template <int E>
 __device__ __forceinline__ uint32_t entry_mask(uint32_t t0, uint32_t t1)
@@ -128,7 +137,7 @@ __device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t s
 
 // MODE: 0 VECTOR, 1 PER_NODE; L = the model's largest ell (planes s_1..s_{L-1})
 template <int MODE, int L>
-__global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
+__global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
 {
     const TrajParams& P = B.T;
     constexpr bool PER_NODE = MODE == 1;
@@ -175,6 +184,7 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
     const uint32_t anyw0 = gbase + (uint32_t)B.any_off;  // any[2][32]
     const uint32_t cw = anyw0 + 256u;                    // constant words FULL, ZERO
     const uint32_t sel0 = gbase + (uint32_t)B.sel_off;   // planes[2]
+    const uint32_t pqt = gbase + (uint32_t)B.pq_off;     // per-quad Philox table
     const uint32_t erec = sbase + B.erec_off;
     const uint32_t rounds = sbase + B.rounds_off;
     const int R = B.n_rounds;
@@ -298,8 +308,12 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
                 uint4 s[3];
 #pragma unroll
                 for (int m = 0; m < L - 1; ++m)
+#if defined(PBN_BS_SKIP_PLANES)
+                    s[m] = make_uint4(rw.x ^ e[m].x, rw.y ^ e[m].y, rw.z ^ e[m].z, rw.w ^ e[m].w);
+#else
                     s[m] = make_uint4(__ballot_sync(FULL, rw.x > e[m].x), __ballot_sync(FULL, rw.y > e[m].y),
                                       __ballot_sync(FULL, rw.z > e[m].z), __ballot_sync(FULL, rw.w > e[m].w));
+#endif
 #pragma unroll
                 for (int m = 0; m < L - 1; ++m) sts128_if(pa + 16u * m, s[m].x, s[m].y, s[m].z, s[m].w, lead);
                 sts128_if(pa + 16u * (L - 1), 0u, 0u, 0u, 0u, lead);              // gamma (flagged quads: below)
@@ -311,29 +325,44 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
                 any |= g0 | g1 | g2 | g3;
                 sts128_if(sel + 16u * (uint32_t)L * (uint32_t)q + 16u * (L - 1), g0, g1, g2, g3, lead);
             };
-            uint4 rw = philox_quad((uint32_t)q0, ps, P.rk);
+            uint4 rw = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)q0), ps, P.rk);
             uint4 e[3];
             for (int qc = q0; qc < qf; qc += 32) {
                 const int qe = min(qf, qc + 32);
                 uint32_t gpend = 0;  // flags of the chunk's quads, newest = bit 0
-                for (int q = qc; q < qe; ++q) {
-                    // the flag vote first: the quad's thresholds, the next
-                    // quad's Philox call and the plane ballots follow it in
-                    // one basic block, so the scheduler overlaps the loads'
-                    // latency and the Philox chain with the ballots
-                    const uint32_t vq = __ballot_sync(FULL, min(min(rw.x, rw.y), min(rw.z, rw.w)) < Tp);
+                // one quad: the flag vote first -- the quad's thresholds, the
+                // next quad's Philox call and the plane ballots follow it in
+                // one basic block, so the scheduler overlaps the loads' latency
+                // and the Philox chain with the ballots
+                auto quad = [&](const int q, const uint4& cur, uint4& next) {
+                    const uint32_t vq = __ballot_sync(FULL, min(min(cur.x, cur.y), min(cur.z, cur.w)) < Tp);
                     thresholds(q, e);
-                    const uint4 rn = philox_quad((uint32_t)(q + 1), ps, P.rk);
-                    planes(q, rw, e);
+#if defined(PBN_BS_SKIP_PHILOX)
+                    next = make_uint4(cur.y * 3u + (uint32_t)q, cur.z ^ cur.x, cur.w + cur.y, cur.x * 5u);
+#else
+                    next = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(q + 1)), ps, P.rk);
+#endif
+                    planes(q, cur, e);
                     asm("{\n\t.reg .u32 f;\n\tmin.u32 f, %1, 1;\n\tmad.lo.u32 %0, %0, 2, f;\n\t}" : "+r"(gpend) : "r"(vq));
+                };
+                // two quads per iteration with the Philox words alternating
+                // between rw and rn: no register rotation moves
+                int q = qc;
+                uint4 rn;
+                for (; q + 1 < qe; q += 2) {
+                    quad(q, rw, rn);
+                    quad(q + 1, rn, rw);
+                }
+                if (q < qe) {
+                    quad(q, rw, rn);
                     rw = rn;
                 }
                 // flagged quads: their gamma words (A4)
                 while (gpend) {
                     const int jb = __ffs((int)gpend) - 1;
                     gpend &= gpend - 1;
-                    const int q = qe - 1 - jb;
-                    gammas(q, philox_quad((uint32_t)q, ps, P.rk));
+                    const int qq = qe - 1 - jb;
+                    gammas(qq, philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)qq), ps, P.rk));
                 }
             }
             if (qf < q1) {  // ragged last quad: padding nodes draw no perturbation
@@ -382,20 +411,51 @@ __global__ void __launch_bounds__(PBN_MAX_THREADS, 1) bitslice_kernel(const __gr
         };
 
         // one interval: statistics of k-1, phase B of k and phase A of k+1
+        // the per-quad Philox table for t_hi of unit step k (all threads;
+        // the caller brackets it with barriers)
+        uint32_t table_thi = 0;
+        auto fill_table = [&](const int64_t k) {
+            table_thi = (uint32_t)((uint64_t)(P.step0 + r_begin - 1 + k) >> 32);
+            for (int q = tid; q <= P.nquads; q += blockDim.x) {
+                const uint4 c = philox_quad_consts((uint32_t)q, table_thi, P.rk);
+                sts128_if(pqt + 16u * (uint32_t)q, c.x, c.y, c.z, c.w, FULL);
+            }
+        };
+        // (PBN_BS_SKIP_A / PBN_BS_SKIP_B: timing-only builds that drop one
+        // phase -- wrong outputs, used to split the step time between them)
+#if defined(PBN_BS_SKIP_A)
+        constexpr bool kA = false;
+#else
+        constexpr bool kA = true;
+#endif
+#if defined(PBN_BS_SKIP_B)
+        constexpr bool kB = false;
+#else
+        constexpr bool kB = true;
+#endif
         auto interval = [&](const int64_t k, auto ob_c, auto nb_c, auto zb_c) {
+            // t_hi of step k + 1 changed (every 2^32 steps): refill the table
+            // first (uniform over the CTA; nobody reads it until phase A)
+            if (k < K && (uint32_t)((uint64_t)(P.step0 + r_begin + k) >> 32) != table_thi) {
+                fill_table(k + 1);
+                __syncthreads();
+            }
             if (k > 1) record(k - 1, decltype(ob_c)::value);
             if (a_first) {
-                if (k < K) phaseA(k + 1, zb_c);
-                phaseB(k, ob_c, nb_c);
+                if (kA && k < K) phaseA(k + 1, zb_c);
+                if (kB) phaseB(k, ob_c, nb_c);
             } else {
-                phaseB(k, ob_c, nb_c);
-                if (k < K) phaseA(k + 1, zb_c);
+                if (kB) phaseB(k, ob_c, nb_c);
+                if (kA && k < K) phaseA(k + 1, zb_c);
             }
             __syncthreads();
         };
         using C0 = std::integral_constant<uint32_t, 0u>;
         using C1 = std::integral_constant<uint32_t, 16u>;
         using C2 = std::integral_constant<uint32_t, 32u>;
+        __syncthreads();  // the previous unit's phase A is done with the table
+        fill_table(1);
+        __syncthreads();
         if (K >= 1) phaseA(1, C1());
         __syncthreads();
         for (int64_t k = 1; k <= K; k += 3) {

@@ -226,6 +226,11 @@ constexpr int kBitsliceMaxTheta = 6;
 constexpr int kBitsliceMaxEll = 4;
 constexpr int kBitsliceMaxNodes = 5460;  // u16 state offsets 48 (i >> 2) + 4 (i & 3) and node ids << 2
 constexpr uint32_t kBitsliceQs = 48;     // bytes between quads: three interleaved state buffers
+// thread budget of the bitslice kernel (its register budget is 65536 / threads)
+#ifndef PBN_BS_THREADS
+#define PBN_BS_THREADS 896
+#endif
+constexpr int kBitsliceMaxWarps = PBN_BS_THREADS / 32;
 struct BitsliceParams {
     TrajParams T;              // T.image = the bitslice image
     uint32_t erec_off;         // image offsets
@@ -234,10 +239,13 @@ struct BitsliceParams {
     int32_t sel_off;           // from the group state base: planes[2][nquads][L] uint4
     int32_t sel_bytes;         // bytes of one plane buffer (16 L nquads)
     int32_t any_off;           // from the group state base: any[2][32] words, then a FULL and a ZERO word
+    int32_t pq_off;            // from the group state base: [nquads + 1] uint4 per-quad Philox values (below)
 };
 // group shared memory of the bitslice kernel (u32 words): 3 state buffers,
-// 2 x 32 any words + 4 constant words, 2 plane buffers of 4 L words per quad
-inline int32_t bitslice_group_words(int32_t n_pad, int32_t L) { return 3 * n_pad + 68 + 2 * L * n_pad; }
+// 2 x 32 any words + 4 constant words, 2 plane buffers of 4 L words per quad,
+// the per-quad Philox table (4 words per quad: the part of rounds 1-2 that
+// depends only on the quad, the key and t_hi, computed once per work unit)
+inline int32_t bitslice_group_words(int32_t n_pad, int32_t L) { return 3 * n_pad + 68 + 2 * L * n_pad + n_pad + 4; }
 const void* pick_bitslice_kernel(int mode, int L);
 // K1's default warps per group for ceil(n/4) quads (pbn_traj.cu)
 int default_group_warps(int nquads);
