@@ -296,7 +296,7 @@ def run_sweep(args, cfg, model, pred):
         def one():
             pbn.pbn_simulate(pm, out, n_chains=chains, steps=args.window, burn_in=args.burn_in,
                              batch=cfg.batch, seed=cfg.sim_seed, pred=pred, init=True, emit_bits=True,
-                             stream=stream)
+                             layout=args.layout, stream=stream)
         for _ in range(args.warmup):
             one()
         torch.cuda.synchronize()
@@ -312,7 +312,7 @@ def run_sweep(args, cfg, model, pred):
         t = statistics.median(ms) / 1e3
         nu = chains * (args.burn_in + args.window) * model.n
         rf = roofline(model, nu, t, 1965.0)
-        print(json.dumps({"sweep": cfg.key, "chains": chains, "n": model.n,
+        print(json.dumps({"sweep": cfg.key, "chains": chains, "n": model.n, "kernel": pbn.pbn_last_kernel(),
                           "steps_per_chain": args.burn_in + args.window,
                           "node_updates_per_s": nu / t, "chain_steps_per_s": chains * (args.burn_in + args.window) / t,
                           "ms": t * 1e3, "ms_best": min(ms) * 1.0, "roofline_frac": rf["frac"], "bound": rf["bound"],
@@ -449,7 +449,8 @@ def main():
         one_step()
         flush.fill_(1)
     torch.cuda.synchronize()
-    kernel_name = {"K1b": "bitslice_kernel (K1b)", "K1": "traj_kernel (K1)", "K1-global": "traj_kernel (K1, global image)",
+    kernel_name = {"K1b": "bitslice_kernel (K1b)", "K1b-global": "bitslice_kernel (K1b, global image)",
+                   "K1": "traj_kernel (K1)", "K1-global": "traj_kernel (K1, global image)",
                    "K1c": "traj_cluster_kernel (K1c)", "K1n": "traj_nodepar_kernel (K1n)"}.get(
         pbn.pbn_last_kernel(), pbn.pbn_last_kernel())
 
@@ -495,7 +496,7 @@ def main():
         except Exception:
             sm_mhz = 1965.0
     rf = roofline(model, node_updates_per_step, avg_kernel_s, sm_mhz, args.geometric)
-    if pbn.pbn_last_kernel() == "K1b":
+    if pbn.pbn_last_kernel() in ("K1b", "K1b-global"):
         db = demand_bitslice(model)
         alu_peak = rf["per_resource"]["alu"]["peak"] * 1e12
         rate = node_updates_per_step / avg_kernel_s

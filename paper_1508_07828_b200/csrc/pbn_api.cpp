@@ -107,7 +107,7 @@ struct pbn_model_s {
     // and every node <= 4 functions (pbn_internal.h)
     uint8_t* d_bs = nullptr;
     uint32_t bs_bytes = 0, bs_erec_off = 0, bs_rounds_off = 0;
-    int32_t bs_rounds = 0, bs_L = 0;
+    int32_t bs_rounds = 0, bs_L = 0, bs_cmax = 0;
     uint32_t geo_last = 0;                // geometric mode: Cg[n-1]
     uint32_t geo_off = 0;                 // geometric mode: byte offset of Cg in the image
     double p = 0.0;
@@ -454,7 +454,7 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
 // model is outside the bit-sliced kernel's shape (theta > 6, ell > 4, too
 // many nodes for u16 offsets).
 bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint8_t>& out, uint32_t* erec_off,
-                          uint32_t* rounds_off, int32_t* n_rounds, int32_t* L_out)
+                          uint32_t* rounds_off, int32_t* n_rounds, int32_t* L_out, int32_t* cmax_out)
 {
     const int32_t n = d->n;
     if (n > pbn::kBitsliceMaxNodes) return false;
@@ -491,38 +491,25 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
     std::vector<std::pair<uint32_t, uint32_t>> rounds;  // (task offset, class)
     for (int32_t c = pbn::kBitsliceMaxTheta; c >= 1; --c) {
         if (cls[c].empty()) continue;
-        const uint32_t stride = c == 6 ? 32u : 16u;
+        const uint32_t T = c <= 5 ? 1u : (1u << c) / 32u;                 // table words
+        const uint32_t stride = c <= 5 ? 16u : c <= 7 ? 32u : 64u;      // kernel: bs_stride
         const size_t cnt = (cls[c].size() + 31) & ~(size_t)31;
         const uint32_t to = B.alloc(stride * cnt, 16);
         for (size_t k = 0; k < cnt; ++k) {
             uint32_t* w = B.u32(to + stride * (uint32_t)k);
+            uint16_t* h = B.u16(to + stride * (uint32_t)k + 4u * T);  // [i << 2 | j, p_0 .. p_{c-1}]
             if (k >= cls[c].size()) {  // dummy task: table 0 contributes nothing
-                w[c == 6 ? 2 : 1] = 1u;  // node 0, function 1 (no perturbation term)
+                h[0] = 1u;  // node 0, function 1 (no perturbation term)
                 continue;
             }
             const int32_t i = cls[c][k].first, j = cls[c][k].second, f = d->fn_off[i] + j;
             const int32_t theta = d->par_off[f + 1] - d->par_off[f];
             // table padded to c index bits: padding parents are the low bits
-            uint32_t T[2] = {0u, 0u};
             for (uint32_t e = 0; e < (1u << c); ++e)
-                T[e >> 5] |= table_bit(d, f, e >> (c - theta)) << (e & 31u);
-            uint32_t p[6] = {0, 0, 0, 0, 0, 0};
+                w[e >> 5] |= table_bit(d, f, e >> (c - theta)) << (e & 31u);
+            h[0] = (uint16_t)(((uint32_t)i << 2) | (uint32_t)j);
             for (int32_t m = 0; m < c; ++m)
-                p[m] = pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u, pbn::kBitsliceQs);
-            const uint32_t ij = ((uint32_t)i << 2) | (uint32_t)j;
-            if (c <= 5) {
-                w[0] = T[0];
-                w[1] = ij | (p[0] << 16);
-                w[2] = p[1] | (p[2] << 16);
-                w[3] = p[3] | (p[4] << 16);
-            } else {
-                w[0] = T[0];
-                w[1] = T[1];
-                w[2] = ij | (p[0] << 16);
-                w[3] = p[1] | (p[2] << 16);
-                w[4] = p[3] | (p[4] << 16);
-                w[5] = p[5];
-            }
+                h[1 + m] = (uint16_t)pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u, pbn::kBitsliceQs);
         }
         for (size_t k = 0; k < cnt; k += 32) rounds.push_back({to + stride * (uint32_t)k, (uint32_t)c});
     }
@@ -538,6 +525,7 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
     *rounds_off = ro;
     *n_rounds = (int32_t)rounds.size();
     *L_out = L;
+    *cmax_out = rounds.empty() ? 1 : (int32_t)rounds.front().second;  // most expensive class first
     return true;
 }
 
@@ -609,7 +597,8 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
     // bit-sliced evaluation image (K1b; VECTOR and PER_NODE semantics)
     if (!geo) {
         std::vector<uint8_t> bs;
-        if (build_bitslice_image(desc, m->Tp, bs, &m->bs_erec_off, &m->bs_rounds_off, &m->bs_rounds, &m->bs_L)) {
+        if (build_bitslice_image(desc, m->Tp, bs, &m->bs_erec_off, &m->bs_rounds_off, &m->bs_rounds, &m->bs_L,
+                                 &m->bs_cmax)) {
             if (cudaMalloc(&m->d_bs, bs.size()) != cudaSuccess ||
                 cudaMemcpy(m->d_bs, bs.data(), bs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
                 if (m->d_bs) cudaFree(m->d_bs);
@@ -805,13 +794,19 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.T = P;
     Bp.T.image = m->d_bs;
     Bp.T.group_words = pbn::bitslice_group_words(P.n_pad, m->bs_L);
-    Bp.T.image_smem_bytes = m->bs_bytes;
+    const size_t group_bytes = (size_t)Bp.T.group_words * 4;
+    if (group_bytes + 64 > (size_t)smem_optin) return PBN_E_USAGE;
+    // the image in shared memory when it fits beside the group state, else
+    // through the read-only global path (L1/L2; PBN_FORCE_GLOBAL_IMAGE=1 forces it)
+    const char* fg = std::getenv("PBN_FORCE_GLOBAL_IMAGE");
+    const bool smem_image = !(fg && fg[0] == '1') && group_bytes + m->bs_bytes + 64 <= (size_t)smem_optin;
+    Bp.T.image_smem_bytes = smem_image ? m->bs_bytes : 0u;
     Bp.erec_off = m->bs_erec_off;
     Bp.rounds_off = m->bs_rounds_off;
     Bp.n_rounds = m->bs_rounds;
     Bp.any_off = 12 * P.n_pad;
     Bp.sel_off = 12 * P.n_pad + 272;
-    Bp.sel_bytes = 4 * m->bs_L * P.n_pad;
+    Bp.sel_bytes = 4 * pbn::bitslice_pv(m->bs_L) * P.n_pad;
     Bp.pq_off = Bp.sel_off + 2 * Bp.sel_bytes;
     // 28 warps (the 72-register budget): C4 6.40e11 vs 6.30e11 node-updates/s at 20
     int W = a->warps_per_group > 0 ? a->warps_per_group : std::min(pbn::kBitsliceMaxWarps, std::max(P.nquads, 1));
@@ -823,18 +818,17 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     plan.stats_warp0 = 0;
     plan.ctas = (int)((P.n_chains + 31) / 32);
     plan.threads = 32 * W;
-    plan.smem_bytes = (size_t)Bp.T.group_words * 4 + m->bs_bytes;
-    plan.image_in_smem = true;
-    if (plan.smem_bytes + 64 > (size_t)smem_optin) return PBN_E_USAGE;
+    plan.smem_bytes = group_bytes + (smem_image ? m->bs_bytes : 0u);
+    plan.image_in_smem = smem_image;
     Bp.T.warps_per_group = W;
     Bp.T.node_warps = plan.node_warps;
     Bp.T.stats_warp0 = 0;
     if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0 || a->workspace_bytes < 0) return PBN_E_USAGE;
-    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : 0, m->bs_L);
+    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : 0, m->bs_L, smem_image, m->bs_cmax);
     const int rc = pbn::launch_group_units(Bp.T, fn, &Bp, plan, m->device, a->schedule, a->chunk_steps, a->workspace,
                                            (size_t)a->workspace_bytes, stream);
     if (rc == -2) return PBN_E_USAGE;
-    if (rc == 0) g_last_kernel = "K1b";
+    if (rc == 0) g_last_kernel = smem_image ? "K1b" : "K1b-global";
     return rc == 0 ? PBN_OK : PBN_E_CUDA;
 }
 
@@ -866,7 +860,7 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     // that fits (C3 4.15e11 -> 5.9e11, C4 5.32e11 -> 6.4e11 node-updates/s);
     // cluster_size = 1 keeps asking for K1 itself
     if (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 && m->d_bs && 2 * groups > sms &&
-        (size_t)pbn::bitslice_group_words(P.n_pad, m->bs_L) * 4 + m->bs_bytes <= limit) {
+        (size_t)pbn::bitslice_group_words(P.n_pad, m->bs_L) * 4 <= limit) {
         const char* nb = std::getenv("PBN_NO_BITSLICE");  // A/B knob: auto without K1b
         if (!(nb && nb[0] == '1')) return simulate_bitslice(m, P, a, stream, smem_optin);
     }

@@ -61,87 +61,118 @@ __device__ __forceinline__ uint4 lds128_state(uint32_t a)
     return v;
 }
 
-// table entry E as a word mask (all ones iff the entry is 1)
-template <int E>
-__device__ __forceinline__ uint32_t entry_mask(uint32_t t0, uint32_t t1)
-{
-    const uint32_t w = E < 32 ? t0 : t1;
-    return (uint32_t)((int32_t)(w << (31 - (E & 31))) >> 31);
-}
-
 // multiplexer tree: the sub-table of entries [B, B + 2^(C-K)) evaluated on
 // the parent words x[K..C-1] (x[0] = parents[0] = the index MSB, reading Q5):
 // x[K] = 0 selects the lower half, 1 the upper -- bit l of the result is the
-// entry at chain l's index
+// entry at chain l's index; table word w holds entries 32 w .. 32 w + 31
 template <int K, int C, int B>
-__device__ __forceinline__ uint32_t mux_tree(uint32_t t0, uint32_t t1, const uint32_t (&x)[C])
+__device__ __forceinline__ uint32_t mux_tree(const uint32_t (&t)[8], const uint32_t (&x)[C])
 {
     if constexpr (K == C) {
-        return entry_mask<B>(t0, t1);
+        return (uint32_t)((int32_t)(t[B >> 5] << (31 - (B & 31))) >> 31);  // entry B as a word mask
     } else {
         constexpr int H = 1 << (C - K - 1);
-        const uint32_t lo = mux_tree<K + 1, C, B>(t0, t1, x);
-        const uint32_t hi = mux_tree<K + 1, C, B + H>(t0, t1, x);
+        const uint32_t lo = mux_tree<K + 1, C, B>(t, x);
+        const uint32_t hi = mux_tree<K + 1, C, B + H>(t, x);
         return (x[K] & hi) | (~x[K] & lo);
     }
 }
 
-// one round of 32 tasks of class C (theta = C parents), lane = task.  The
-// node's plane words are at pl + 16 m (m = 0..L-2: s_{m+1}; m = L-1:
-// gamma); `cw` holds the constant words FULL (cw) and ZERO (cw + 4) that
-// stand in for s_0 and s_L, so every load is unconditional.
-template <int C, int MODE, int L, uint32_t OB, uint32_t NB>
-__device__ __forceinline__ void bs_round(uint32_t ta, uint32_t gbase, uint32_t sel, uint32_t cw, uint32_t M)
-{
-    uint32_t t0, t1 = 0, w0, w1, w2, w3 = 0;
-    if constexpr (C <= 5) {
-        const uint4 r = lds128_ro(ta);
-        t0 = r.x;
-        w0 = r.y;
-        w1 = r.z;
-        w2 = r.w;
-    } else {
-        const uint4 r = lds128_ro(ta);
-        const uint2 r2 = lds64_ro(ta + 16u);
-        t0 = r.x;
-        t1 = r.y;
-        w0 = r.z;
-        w1 = r.w;
-        w2 = r2.x;
-        w3 = r2.y;
+// The bitslice image, staged in shared memory (SMEM) or read through the
+// read-only global path (large models, e.g. C5: tasks are read coalesced,
+// a round's 32 records consecutive; thresholds and round records are warp-
+// uniform broadcasts).  Offsets are bytes from the image start.
+template <bool SMEM>
+struct BImg {
+    const uint8_t* g;  // global image
+    uint32_t s;        // shared address of the staged image
+    __device__ __forceinline__ uint4 ld128(uint32_t off) const
+    {
+        if (SMEM) return lds128_ro(s + off);
+        return __ldg(reinterpret_cast<const uint4*>(g + off));
     }
-    const uint32_t pw[6] = {w0 >> 16, w1 & 0xFFFFu, w1 >> 16, w2 & 0xFFFFu, w2 >> 16, w3 & 0xFFFFu};
+    __device__ __forceinline__ uint2 ld64(uint32_t off) const
+    {
+        if (SMEM) return lds64_ro(s + off);
+        return __ldg(reinterpret_cast<const uint2*>(g + off));
+    }
+};
+
+// record stride of task class c (table words, then the u16 list
+// [i << 2 | j, p_0 .. p_{c-1}]; pbn_internal.h)
+__host__ __device__ constexpr uint32_t bs_stride(int c) { return c <= 5 ? 16u : c <= 7 ? 32u : 64u; }
+
+// plane vectors per quad: NP selection-index planes (b0 = bit 0 of j, b1 =
+// bit 1) and the gamma vector
+template <int L>
+struct Planes {
+    static constexpr int NP = L >= 3 ? 2 : L == 2 ? 1 : 0;
+    static constexpr int PV = NP + 1;
+};
+
+// one round of 32 tasks of class C (theta = C parents), lane = task.  ob / nb
+// are the byte offsets of the old / new state buffer (uniform); the node's
+// plane words are at pl + 16 m (m < NP: b_m; m = NP: gamma).
+template <int C, int MODE, int L, bool SMEM>
+__device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uint32_t gob, uint32_t gnb, uint32_t sel,
+                                         uint32_t M)
+{
+    constexpr int T = C <= 5 ? 1 : (1 << C) / 32;      // table words
+    constexpr int NV = (4 * T + 2 * (C + 1) + 15) / 16;  // 16-byte vectors of the record
+    constexpr int NP = Planes<L>::NP, PV = Planes<L>::PV;
+    uint32_t w[4 * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const uint4 r = img.ld128(ta + 16u * v);
+        w[4 * v] = r.x;
+        w[4 * v + 1] = r.y;
+        w[4 * v + 2] = r.z;
+        w[4 * v + 3] = r.w;
+    }
+    uint32_t t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = k < T ? w[k] : 0u;
+    // u16 k of the list (0: i << 2 | j; 1 + m: parent m)
+    auto u16 = [&](int k) -> uint32_t {
+        const uint32_t x = w[T + (k >> 1)];
+        return (k & 1) ? x >> 16 : x & 0xFFFFu;
+    };
     uint32_t x[C];
 #pragma unroll
-    for (int m = 0; m < C; ++m) x[m] = lds32_state(gbase + pw[m] + OB);
-    const uint32_t F = mux_tree<0, C, 0>(t0, t1, x);
-    const uint32_t i = (w0 & 0xFFFFu) >> 2, j = w0 & 3u;
-    const uint32_t pl = sel + 16u * (uint32_t)L * (i >> 2) + 4u * (i & 3u);
-    // selection plane of function j: s_j & ~s_{j+1} (s_0 = all chains, s_L = none)
-    const uint32_t s_lo = lds32_state(j == 0 ? cw : pl + 16u * (j - 1u));
-    const uint32_t s_hi = lds32_state(j == (uint32_t)(L - 1) ? cw + 4u : pl + 16u * j);
-    const uint32_t gam = lds32_state(pl + 16u * (uint32_t)(L - 1));
-    const uint32_t out = gbase + state_off(i, kBitsliceQs);
-    const uint32_t old = lds32_state(out + OB);
+    for (int m = 0; m < C; ++m) x[m] = lds32_state(gob + u16(1 + m));
+    const uint32_t F = mux_tree<0, C, 0>(t, x);
+    const uint32_t ij = u16(0);
+    const uint32_t i = ij >> 2, j = ij & 3u;
+    const uint32_t pl = sel + 16u * (uint32_t)PV * (i >> 2) + 4u * (i & 3u);
+    // selection plane of function j: the chains whose index bits equal j's
+    const uint32_t b0 = NP >= 1 ? lds32_state(pl) : 0u;
+    const uint32_t b1 = NP >= 2 ? lds32_state(pl + 16u) : 0u;
+    const uint32_t gam = lds32_state(pl + 16u * NP);
+    const uint32_t m0 = (j & 1u) - 1u, m1 = ((j >> 1) & 1u) - 1u;  // all ones where the bit of j is 0
+    const uint32_t sj = (b0 ^ m0) & (NP >= 2 ? (b1 ^ m1) : m1);
+    const uint32_t out = state_off(i, kBitsliceQs);
+    const uint32_t old = lds32_state(gob + out);
     const uint32_t first = j == 0 ? FULL : 0u;  // function 0 carries the perturbation term
     uint32_t c;
     if (MODE == 1) {  // PER_NODE: chains with gamma_i take NOT s_i
-        c = (F & s_lo & ~s_hi & ~gam) | (~old & gam & first);
+        c = (F & sj & ~gam) | (~old & gam & first);
     } else {          // VECTOR: chains with any gamma take s XOR gamma
-        c = (F & s_lo & ~s_hi & ~M) | ((old ^ gam) & M & first);
+        c = (F & sj & ~M) | ((old ^ gam) & M & first);
     }
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(out + NB),
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(gnb + out),
                  "r"(c)
                  : "memory");
 }
 
-// MODE: 0 VECTOR, 1 PER_NODE; L = the model's largest ell (planes s_1..s_{L-1})
-template <int MODE, int L>
+// MODE: 0 VECTOR, 1 PER_NODE; L = the model's largest ell; SMEM: image staged;
+// CMAX: the largest task class (6 or 8)
+template <int MODE, int L, bool SMEM, int CMAX>
 __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
 {
     const TrajParams& P = B.T;
     constexpr bool PER_NODE = MODE == 1;
     constexpr uint32_t QS = kBitsliceQs;
+    constexpr int NP = Planes<L>::NP, PV = Planes<L>::PV;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
 
@@ -151,10 +182,10 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     const int W = P.warps_per_group;
     const int n = P.n;
     const uint32_t gbase = smem_u32(smem);
-    const uint32_t sbase = gbase + 4u * (uint32_t)P.group_words;  // image base
+    const uint32_t sbase = gbase + 4u * (uint32_t)P.group_words;  // staged image base
 
     // ---- A1: stage the image into shared memory (bulk async copy) ----
-    {
+    if (SMEM) {
         const uint32_t bar = smem_u32(&mbar);
         if (tid == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
@@ -178,20 +209,18 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             "@!p bra WAIT_%=;\n}\n" ::"r"(bar)
             : "memory");
     }
+    BImg<SMEM> img;
+    img.g = P.image;
+    img.s = sbase;
 
     const bool leader = lane == 0;
     const uint32_t lead = leader ? FULL : 0u;
     const uint32_t anyw0 = gbase + (uint32_t)B.any_off;  // any[2][32]
-    const uint32_t cw = anyw0 + 256u;                    // constant words FULL, ZERO
     const uint32_t sel0 = gbase + (uint32_t)B.sel_off;   // planes[2]
     const uint32_t pqt = gbase + (uint32_t)B.pq_off;     // per-quad Philox table
-    const uint32_t erec = sbase + B.erec_off;
-    const uint32_t rounds = sbase + B.rounds_off;
+    const uint32_t erec = B.erec_off;
+    const uint32_t rounds = B.rounds_off;
     const int R = B.n_rounds;
-    if (tid == 0) {
-        sts32(cw, FULL);
-        sts32(cw + 4u, 0u);
-    }
 
     const int NW = P.node_warps;
     const int q0 = wg < NW ? (int)((int64_t)wg * P.nquads / NW) : P.nquads;
@@ -287,43 +316,56 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         // unit step k = 1..K is step r = r_begin - 1 + k; S_k in buffer k % 3
         const int64_t K = r_end - r_begin + 1;
 
-        // ---- phase A of unit step k: planes -> planes[k & 1], zero S_k's buffer ZB ----
-        auto phaseA = [&](const int64_t k, auto zb_c) {
-            constexpr uint32_t ZB = decltype(zb_c)::value;
+        // ---- phase A of unit step k: planes -> planes[k & 1], zero S_k's buffer (byte offset zb) ----
+        auto phaseA = [&](const int64_t k, const uint32_t zb) {
             const uint64_t t = (uint64_t)(P.step0 + r_begin - 1 + k);
             const uint32_t t_lo = (uint32_t)t, t_hi = (uint32_t)(t >> 32);
             const uint32_t sel = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes;
+            const uint32_t gzb = gbase + zb;
             uint32_t any = 0;
             const PhiloxStep ps = philox_step(chain, t_lo, t_hi, P.rk);
             const int qf = (full_quads || q1 == q0) ? q1 : q1 - 1;
-            // quad q's record: L vectors of 16 bytes at sel + 16 L q -- the planes
-            // s_1..s_{L-1} of its 4 nodes, then their gamma words
+            // quad q's record: PV vectors of 16 bytes at sel + 16 PV q -- the
+            // selection-index planes b_0 (b_1) of its 4 nodes, then their gamma
+            // words: chain l picks function j = #{m : u_l > E_m}, b_0 = bit 0 of j
+            // (the parity of the compares, the thresholds ascending), b_1 = bit 1
+            // (= [u > E_2])
             auto thresholds = [&](const int q, uint4 (&e)[3]) {
                 const uint32_t ea = erec + 16u * (uint32_t)(L - 1) * (uint32_t)q;
 #pragma unroll
-                for (int m = 0; m < L - 1; ++m) e[m] = lds128_ro(ea + 16u * m);
+                for (int m = 0; m < L - 1; ++m) e[m] = img.ld128(ea + 16u * m);
             };
             auto planes = [&](const int q, const uint4 rw, const uint4 (&e)[3]) {
-                const uint32_t pa = sel + 16u * (uint32_t)L * (uint32_t)q;
-                uint4 s[3];
+                const uint32_t pa = sel + 16u * (uint32_t)PV * (uint32_t)q;
+                const uint32_t u[4] = {rw.x, rw.y, rw.z, rw.w};
+                uint32_t pb0[4], pb1[4];
 #pragma unroll
-                for (int m = 0; m < L - 1; ++m)
-#if defined(PBN_BS_SKIP_PLANES)
-                    s[m] = make_uint4(rw.x ^ e[m].x, rw.y ^ e[m].y, rw.z ^ e[m].z, rw.w ^ e[m].w);
-#else
-                    s[m] = make_uint4(__ballot_sync(FULL, rw.x > e[m].x), __ballot_sync(FULL, rw.y > e[m].y),
-                                      __ballot_sync(FULL, rw.z > e[m].z), __ballot_sync(FULL, rw.w > e[m].w));
-#endif
-#pragma unroll
-                for (int m = 0; m < L - 1; ++m) sts128_if(pa + 16u * m, s[m].x, s[m].y, s[m].z, s[m].w, lead);
-                sts128_if(pa + 16u * (L - 1), 0u, 0u, 0u, 0u, lead);              // gamma (flagged quads: below)
-                sts128_if(gbase + QS * (uint32_t)q + ZB, 0u, 0u, 0u, 0u, lead);  // S_k's words, OR-ed in phase B
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t E1 = k == 0 ? e[0].x : k == 1 ? e[0].y : k == 2 ? e[0].z : e[0].w;
+                    const uint32_t E2 = k == 0 ? e[1].x : k == 1 ? e[1].y : k == 2 ? e[1].z : e[1].w;
+                    const uint32_t E3 = k == 0 ? e[2].x : k == 1 ? e[2].y : k == 2 ? e[2].z : e[2].w;
+                    if (L == 2) {
+                        pb0[k] = __ballot_sync(FULL, u[k] > E1);
+                    } else if (L == 3) {
+                        const bool p2 = u[k] > E2;
+                        pb0[k] = __ballot_sync(FULL, (u[k] > E1) != p2);
+                        pb1[k] = __ballot_sync(FULL, p2);
+                    } else if (L == 4) {
+                        const bool p2 = u[k] > E2;
+                        pb0[k] = __ballot_sync(FULL, ((u[k] > E1) != p2) != (u[k] > E3));
+                        pb1[k] = __ballot_sync(FULL, p2);
+                    }
+                }
+                if (NP >= 1) sts128_if(pa, pb0[0], pb0[1], pb0[2], pb0[3], lead);
+                if (NP >= 2) sts128_if(pa + 16u, pb1[0], pb1[1], pb1[2], pb1[3], lead);
+                sts128_if(pa + 16u * NP, 0u, 0u, 0u, 0u, lead);               // gamma (flagged quads: below)
+                sts128_if(gzb + QS * (uint32_t)q, 0u, 0u, 0u, 0u, lead);  // S_k's words, OR-ed in phase B
             };
             auto gammas = [&](const int q, const uint4 rq) {
                 const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
                 const uint32_t g2 = __ballot_sync(FULL, rq.z < Tp), g3 = __ballot_sync(FULL, rq.w < Tp);
                 any |= g0 | g1 | g2 | g3;
-                sts128_if(sel + 16u * (uint32_t)L * (uint32_t)q + 16u * (L - 1), g0, g1, g2, g3, lead);
+                sts128_if(sel + 16u * (uint32_t)PV * (uint32_t)q + 16u * NP, g0, g1, g2, g3, lead);
             };
             uint4 rw = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)q0), ps, P.rk);
             uint4 e[3];
@@ -376,31 +418,34 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             if (!PER_NODE && leader) sts32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * wg, any);
         };
 
-        // ---- phase B of unit step k: S_k (buffer NB) from S_{k-1} (OB) and planes[k & 1] ----
-        auto phaseB = [&](const int64_t k, auto ob_c, auto nb_c) {
-            constexpr uint32_t OB = decltype(ob_c)::value;
-            constexpr uint32_t NB = decltype(nb_c)::value;
+        // ---- phase B of unit step k: S_k (buffer nb) from S_{k-1} (ob) and planes[k & 1] ----
+        auto phaseB = [&](const int64_t k, const uint32_t ob, const uint32_t nb) {
             const uint32_t sel = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes;
+            const uint32_t gob = gbase + ob, gnb = gbase + nb;
             uint32_t M = 0;
             if (!PER_NODE)
                 M = __reduce_or_sync(FULL, lane < W ? lds32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * lane) : 0u) & vmask;
             for (int m = 0; m * W < R; ++m) {
                 const int rr_i = (m & 1) ? (m + 1) * W - 1 - wg : m * W + wg;
                 if (rr_i >= R) continue;
-                const uint2 rr = lds64_ro(rounds + 8u * (uint32_t)rr_i);
-                const uint32_t ta = sbase + rr.x + (uint32_t)lane * (rr.y == 6u ? 32u : 16u);
+                const uint2 rr = img.ld64(rounds + 8u * (uint32_t)rr_i);
+                const uint32_t ta = rr.x + (uint32_t)lane * bs_stride((int)rr.y);
                 switch (rr.y) {
-                    case 1: bs_round<1, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
-                    case 2: bs_round<2, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
-                    case 3: bs_round<3, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
-                    case 4: bs_round<4, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
-                    case 5: bs_round<5, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
-                    default: bs_round<6, MODE, L, OB, NB>(ta, gbase, sel, cw, M); break;
+                    case 1: bs_round<1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 2: bs_round<2, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 3: bs_round<3, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 4: bs_round<4, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 5: bs_round<5, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 6: bs_round<6, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    // classes 7 and 8 only in the CMAX = 8 kernels: their trees'
+                    // registers would otherwise spill the theta <= 6 kernels
+                    case 7: if constexpr (CMAX >= 7) bs_round<CMAX >= 7 ? 7 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    default: if constexpr (CMAX >= 8) bs_round<CMAX >= 8 ? 8 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
                 }
             }
         };
 
-        // statistics of unit step k (S_k in buffer BUF), statistics warps
+        // statistics of unit step k (S_k in the buffer at byte offset buf), statistics warps
         auto record = [&](const int64_t k, const uint32_t buf) {
             const int64_t r = r_begin - 1 + k;
             if (stats && r > P.burn_in) {
@@ -410,7 +455,6 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             }
         };
 
-        // one interval: statistics of k-1, phase B of k and phase A of k+1
         // the per-quad Philox table for t_hi of unit step k (all threads;
         // the caller brackets it with barriers)
         uint32_t table_thi = 0;
@@ -433,37 +477,36 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
 #else
         constexpr bool kB = true;
 #endif
-        auto interval = [&](const int64_t k, auto ob_c, auto nb_c, auto zb_c) {
+        __syncthreads();  // the previous unit's phase A is done with the table
+        fill_table(1);
+        __syncthreads();
+        if (K >= 1) phaseA(1, 16u);
+        __syncthreads();
+        // one interval per step k: statistics of k-1, phase B of k and phase A
+        // of k+1; buffers ob = S_{k-1}, nb = S_k, zb = S_{k+1} rotate (uniform)
+        uint32_t ob = 0u, nb = 16u, zb = 32u;
+        for (int64_t k = 1; k <= K; ++k) {
             // t_hi of step k + 1 changed (every 2^32 steps): refill the table
             // first (uniform over the CTA; nobody reads it until phase A)
             if (k < K && (uint32_t)((uint64_t)(P.step0 + r_begin + k) >> 32) != table_thi) {
                 fill_table(k + 1);
                 __syncthreads();
             }
-            if (k > 1) record(k - 1, decltype(ob_c)::value);
+            if (k > 1) record(k - 1, ob);
             if (a_first) {
-                if (kA && k < K) phaseA(k + 1, zb_c);
-                if (kB) phaseB(k, ob_c, nb_c);
+                if (kA && k < K) phaseA(k + 1, zb);
+                if (kB) phaseB(k, ob, nb);
             } else {
-                if (kB) phaseB(k, ob_c, nb_c);
-                if (kA && k < K) phaseA(k + 1, zb_c);
+                if (kB) phaseB(k, ob, nb);
+                if (kA && k < K) phaseA(k + 1, zb);
             }
             __syncthreads();
-        };
-        using C0 = std::integral_constant<uint32_t, 0u>;
-        using C1 = std::integral_constant<uint32_t, 16u>;
-        using C2 = std::integral_constant<uint32_t, 32u>;
-        __syncthreads();  // the previous unit's phase A is done with the table
-        fill_table(1);
-        __syncthreads();
-        if (K >= 1) phaseA(1, C1());
-        __syncthreads();
-        for (int64_t k = 1; k <= K; k += 3) {
-            interval(k, C0(), C1(), C2());
-            if (k + 1 <= K) interval(k + 1, C1(), C2(), C0());
-            if (k + 2 <= K) interval(k + 2, C2(), C0(), C1());
+            const uint32_t t3 = ob;
+            ob = nb;
+            nb = zb;
+            zb = t3;
         }
-        const uint32_t cur = 16u * (uint32_t)(K % 3);  // S_K's buffer
+        const uint32_t cur = ob;  // S_K's buffer (K >= 1), buffer 0 for K = 0
         if (K >= 1) record(K, cur);
 
         if (!last_chunk) {
@@ -501,19 +544,29 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     }
 }
 
-template <int MODE>
+template <int MODE, bool SMEM, int CMAX>
 const void* pick_L(int L)
 {
     switch (L) {
-        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1>);
-        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2>);
-        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3>);
-        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4>);
+        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1, SMEM, CMAX>);
+        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2, SMEM, CMAX>);
+        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3, SMEM, CMAX>);
+        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4, SMEM, CMAX>);
     }
+}
+
+template <int MODE>
+const void* pick_mode(int L, bool smem_image, int cmax)
+{
+    if (smem_image) return cmax <= 6 ? pick_L<MODE, true, 6>(L) : pick_L<MODE, true, 8>(L);
+    return cmax <= 6 ? pick_L<MODE, false, 6>(L) : pick_L<MODE, false, 8>(L);
 }
 
 }  // namespace
 
-const void* pick_bitslice_kernel(int mode, int L) { return mode == 1 ? pick_L<1>(L) : pick_L<0>(L); }
+const void* pick_bitslice_kernel(int mode, int L, bool smem_image, int cmax)
+{
+    return mode == 1 ? pick_mode<1>(L, smem_image, cmax) : pick_mode<0>(L, smem_image, cmax);
+}
 
 }  // namespace pbn

@@ -195,34 +195,37 @@ int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem
 // Bit-sliced evaluation launch (pbn_bitslice.cu, K1b): one 32-chain group
 // per CTA with K1's bit-sliced state words (THREE interleaved buffers, quads
 // 48 bytes apart: state_off(i, 48) + 16 b), the node step split in two phases:
-//   A  lane = chain: Philox words, and per node the selection planes
-//      s_m = ballot(u > E_m), m = 1..L-1 (and gamma = ballot(u < T_p) for the
-//      ~1 % of quads where some chain drew one), stored per quad as L
-//      16-byte vectors (s_1..s_{L-1}, gamma of its 4 nodes); each warp
-//      zeroes its quads' words of the step's state buffer
+//   A  lane = chain: Philox words, and per node the bits of the selected
+//      function's index j = #{m : u > E_m} as ballots -- b_0 (bit 0: the
+//      parity of the compares) and, for L >= 3, b_1 (bit 1: [u > E_2]) --
+//      and gamma = ballot(u < T_p) for the ~1 % of quads where some chain drew
+//      one; stored per quad as PV = NP + 1 16-byte vectors (b_0, [b_1], gamma
+//      of its 4 nodes; NP = 0, 1, 2 for L = 1, 2, >= 3); each warp zeroes its
+//      quads' words of the step's state buffer
 //   B  lane = (node, function) task: the function is evaluated for all 32
 //      chains at once on the parents' bit-sliced words (a multiplexer tree
-//      over its truth table), masked by its selection plane s_j & ~s_{j+1}
-//      and OR-ed into the node's new word (the chains' selections are
+//      over its truth table), masked by the chains whose index bits equal
+//      its j and OR-ed into the node's new word (the chains' selections are
 //      disjoint, so the OR of all tasks of a node is the new word)
 // Phase A needs no state, so A of step t+1 runs in the same interval as B of
 // step t (planes and any words double-buffered by step parity, state
 // triple-buffered): one barrier per step.
-// BITSLICE image (staged whole into shared memory, byte offsets from its start):
+// BITSLICE image (staged whole into shared memory when it fits with the
+// group state, else read through the read-only global path; byte offsets
+// from its start):
 //   erec   [nquads][L-1] uint4: E_{m+1} of the quad's 4 nodes (0xFFFFFFFF
-//          when m + 1 >= ell or the node is padding: the plane is 0)
-//   tasks  per class c = max(theta, 1) = 1..6, padded to whole rounds of 32
-//          (dummy tasks: table 0), stride 16 bytes (c <= 5) or 32 (c = 6):
-//            c <= 5: {t, (i << 2 | j) | p0 << 16, p1 | p2 << 16, p3 | p4 << 16}
-//            c = 6:  {t0, t1, (i << 2 | j) | p0 << 16, p1 | p2 << 16}
-//                    {p3 | p4 << 16, p5, 0, 0}
-//          t = the 2^c-entry table, entry e at bit e (t1: entries 32..63),
-//          idx = sum_m x(p_m) 2^(c-1-m) (parents[0] the MSB, reading Q5);
-//          i = node, j = function index within the node, p_m =
-//          state_off(parent m, 48) (u16 bytes; theta = 0 pads one ignored parent)
+//          when m + 1 >= ell or the node is padding: the compare is false)
+//   tasks  per class c = max(theta, 1) = 1..8, padded to whole rounds of 32
+//          (dummy tasks: table 0, node 0, j 1), each record the 2^c-entry
+//          table in T = max(1, 2^c / 32) words (entry e at bit e & 31 of word
+//          e >> 5), then the u16 list [i << 2 | j, p_0 .. p_{c-1}]; stride 16
+//          bytes (c <= 5), 32 (c = 6, 7), 64 (c = 8).  idx = sum_m x(p_m)
+//          2^(c-1-m) (parents[0] the MSB, reading Q5); i = node, j = function
+//          index within the node, p_m = state_off(parent m, 48) (theta = 0
+//          pads one ignored parent)
 //   rounds [n_rounds] uint2 {byte offset of the round's first task, c},
 //          most expensive class first (warps take them in snake order)
-constexpr int kBitsliceMaxTheta = 6;
+constexpr int kBitsliceMaxTheta = 8;
 constexpr int kBitsliceMaxEll = 4;
 constexpr int kBitsliceMaxNodes = 5460;  // u16 state offsets 48 (i >> 2) + 4 (i & 3) and node ids << 2
 constexpr uint32_t kBitsliceQs = 48;     // bytes between quads: three interleaved state buffers
@@ -236,17 +239,22 @@ struct BitsliceParams {
     uint32_t erec_off;         // image offsets
     uint32_t rounds_off;
     int32_t n_rounds;
-    int32_t sel_off;           // from the group state base: planes[2][nquads][L] uint4
-    int32_t sel_bytes;         // bytes of one plane buffer (16 L nquads)
-    int32_t any_off;           // from the group state base: any[2][32] words, then a FULL and a ZERO word
+    int32_t sel_off;           // from the group state base: planes[2][nquads][PV] uint4
+    int32_t sel_bytes;         // bytes of one plane buffer (16 PV nquads)
+    int32_t any_off;           // from the group state base: any[2][32] words
     int32_t pq_off;            // from the group state base: [nquads + 1] uint4 per-quad Philox values (below)
 };
+// plane vectors per quad for the model's largest ell L
+inline int32_t bitslice_pv(int32_t L) { return (L >= 3 ? 2 : L == 2 ? 1 : 0) + 1; }
 // group shared memory of the bitslice kernel (u32 words): 3 state buffers,
-// 2 x 32 any words + 4 constant words, 2 plane buffers of 4 L words per quad,
-// the per-quad Philox table (4 words per quad: the part of rounds 1-2 that
+// 2 x 32 any words + 4 spare, 2 plane buffers of 4 PV words per quad, the
+// per-quad Philox table (4 words per quad: the part of rounds 1-2 that
 // depends only on the quad, the key and t_hi, computed once per work unit)
-inline int32_t bitslice_group_words(int32_t n_pad, int32_t L) { return 3 * n_pad + 68 + 2 * L * n_pad + n_pad + 4; }
-const void* pick_bitslice_kernel(int mode, int L);
+inline int32_t bitslice_group_words(int32_t n_pad, int32_t L)
+{
+    return 3 * n_pad + 68 + 2 * bitslice_pv(L) * n_pad + n_pad + 4;
+}
+const void* pick_bitslice_kernel(int mode, int L, bool smem_image, int cmax);
 // K1's default warps per group for ceil(n/4) quads (pbn_traj.cu)
 int default_group_warps(int nquads);
 

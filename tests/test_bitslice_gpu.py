@@ -70,12 +70,29 @@ def bs_models():
                        [int(b) for b in rng.integers(0, 2, 8)], 1.0)])
     yield "boolean_network_ell1", model_from_lists(33, 1e-3, nodes), Predicate(
         np.array([0], np.uint16), np.array([1], np.uint8))
+    yield "theta_7_classes", random_pbn(48, 1, 4, 4, 7, 0.004, seed=6), Predicate(
+        np.array([5, 6], np.uint16), np.array([1, 0], np.uint8))
+    yield "theta_8_classes", random_pbn(61, 2, 4, 6, 8, 0.004, seed=7), Predicate(
+        np.array([60], np.uint16), np.array([1], np.uint8))
+    yield "ell3_theta1_8", random_pbn(130, 1, 3, 1, 8, 0.002, seed=13), Predicate(
+        np.array([3, 129], np.uint16), np.array([0, 1], np.uint8))
 
 
 @pytest.mark.parametrize("per_node", [False, True])
 @pytest.mark.parametrize("name,model,pred", list(bs_models()), ids=[e[0] for e in bs_models()])
 def test_models_all_chains(pbn, name, model, pred, per_node):
     full_compare(pbn, model, pred, n_chains=45, steps=777, burn_in=123, seed=17, batch=50, per_node=per_node)
+
+
+@pytest.mark.parametrize("per_node", [False, True])
+@pytest.mark.parametrize("name", ["n150_all_classes", "theta_8_classes", "ell3_theta1_8"])
+def test_models_global_image(pbn, name, per_node, monkeypatch):
+    """The image read through L1/L2 instead of staged (the C5 shape):
+    PBN_FORCE_GLOBAL_IMAGE=1 forces it for small models."""
+    model, pred = {k: (m, p) for k, m, p in bs_models()}[name]
+    monkeypatch.setenv("PBN_FORCE_GLOBAL_IMAGE", "1")
+    full_compare(pbn, model, pred, n_chains=70, steps=555, burn_in=45, seed=23, batch=37, per_node=per_node)
+    assert pbn.pbn_last_kernel() == "K1b-global"
 
 
 @pytest.mark.parametrize("per_node", [False, True])
@@ -173,9 +190,9 @@ def test_large_configs_sampled_chains(pbn, key):
 
 
 def test_outside_shape_is_refused(pbn):
-    """theta > 6 (or ell > 4, or the geometric stream) has no K1b image: the
+    """theta > 8 (or ell > 4, or the geometric stream) has no K1b image: the
     forced layout fails loudly instead of falling back."""
-    model = random_pbn(48, 1, 4, 4, 7, 0.004, seed=6)
+    model = random_pbn(64, 1, 3, 6, 10, 0.002, seed=3)
     pm = pbn.pbn_load(model)
     with pytest.raises(Exception):
         gpu_run(pm, model, Predicate(np.array([5], np.uint16), np.array([1], np.uint8)), n_chains=40, steps=10,
