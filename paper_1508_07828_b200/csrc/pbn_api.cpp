@@ -594,10 +594,11 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
         delete m;
         return cuda_status(e, err, errlen, "cudaMemcpy(image)");
     }
-    // bit-sliced evaluation image (K1b; VECTOR and PER_NODE semantics)
-    if (!geo) {
+    // bit-sliced evaluation image (K1b; every semantics -- geometric: the
+    // thresholds without the T_p share, gamma from the skip stream)
+    {
         std::vector<uint8_t> bs;
-        if (build_bitslice_image(desc, m->Tp, bs, &m->bs_erec_off, &m->bs_rounds_off, &m->bs_rounds, &m->bs_L,
+        if (build_bitslice_image(desc, Tsel, bs, &m->bs_erec_off, &m->bs_rounds_off, &m->bs_rounds, &m->bs_L,
                                  &m->bs_cmax)) {
             if (cudaMalloc(&m->d_bs, bs.size()) != cudaSuccess ||
                 cudaMemcpy(m->d_bs, bs.data(), bs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -783,8 +784,9 @@ static pbn_status fill_traj_params(pbn_model m, const pbn_sim_args* a, const pbn
 }
 
 // K1b launch: one 32-chain group per CTA (persistent schedule as K1), the
-// bitslice image staged into shared memory.  PBN_E_USAGE when the model has
-// no bitslice image (theta > 6, ell > 4, geometric mode) or it does not fit.
+// bitslice image staged into shared memory or read through L1/L2.
+// PBN_E_USAGE when the model has no bitslice image (theta > 8, ell > 4,
+// n > 5460) or its group state does not fit.
 static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const pbn_sim_args* a, void* stream,
                                     int smem_optin)
 {
@@ -824,7 +826,8 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.T.node_warps = plan.node_warps;
     Bp.T.stats_warp0 = 0;
     if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0 || a->workspace_bytes < 0) return PBN_E_USAGE;
-    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : 0, m->bs_L, smem_image, m->bs_cmax);
+    if (P.geometric) Bp.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->geo_off);
+    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, smem_image, m->bs_cmax);
     const int rc = pbn::launch_group_units(Bp.T, fn, &Bp, plan, m->device, a->schedule, a->chunk_steps, a->workspace,
                                            (size_t)a->workspace_bytes, stream);
     if (rc == -2) return PBN_E_USAGE;

@@ -1,0 +1,8 @@
+// pbn_bitslice_m2.cu -- K1b kernels of MODE 2 (VECTOR with the geometric-skip stream); see pbn_bitslice_kernel.cuh.
+#include "pbn_bitslice_kernel.cuh"
+
+namespace pbn {
+
+const void* pick_bitslice_kernel_mode2(int L, bool smem_image, int cmax) { return pick_mode<2>(L, smem_image, cmax); }
+
+}  // namespace pbn

@@ -243,6 +243,7 @@ struct BitsliceParams {
     int32_t sel_bytes;         // bytes of one plane buffer (16 PV nquads)
     int32_t any_off;           // from the group state base: any[2][32] words
     int32_t pq_off;            // from the group state base: [nquads + 1] uint4 per-quad Philox values (below)
+    const uint32_t* geo_table; // geometric mode: Cg[0..n-1] (the main image's copy, global memory)
 };
 // plane vectors per quad for the model's largest ell L
 inline int32_t bitslice_pv(int32_t L) { return (L >= 3 ? 2 : L == 2 ? 1 : 0) + 1; }

@@ -410,11 +410,26 @@ __device__ __forceinline__ uint32_t node_word(const Img<SMEM>& img, const uint4 
 // gamma word of its node (gam = buffer base, word i at gam + 4 i).  Returns
 // the ballot of lanes with gamma(t) != 0.  The first word decides "any
 // flip" with one compare (G(v_0) < n iff v_0 < Cg[n-1]).
+template <bool SMEM, typename GamAddr>
+__device__ __forceinline__ uint32_t geometric_gamma_at(const Img<SMEM>& img, uint32_t geo, int n, float inv_lnq,
+                                                       uint32_t chain, uint32_t t_lo, uint32_t t_hi,
+                                                       const uint32_t* __restrict__ rk, GamAddr gam_of, uint32_t lmask,
+                                                       bool valid);
 template <bool SMEM>
 __device__ __forceinline__ uint32_t geometric_gamma(const Img<SMEM>& img, uint32_t geo, int n, float inv_lnq,
                                                     uint32_t chain, uint32_t t_lo, uint32_t t_hi,
                                                     const uint32_t* __restrict__ rk, uint32_t gam, uint32_t lmask,
                                                     bool valid)
+{
+    return geometric_gamma_at(img, geo, n, inv_lnq, chain, t_lo, t_hi, rk,
+                              [gam](uint32_t k) { return gam + 4u * k; }, lmask, valid);
+}
+// the same with node k's gamma word at gam_of(k) (K1b: inside the plane vectors)
+template <bool SMEM, typename GamAddr>
+__device__ __forceinline__ uint32_t geometric_gamma_at(const Img<SMEM>& img, uint32_t geo, int n, float inv_lnq,
+                                                       uint32_t chain, uint32_t t_lo, uint32_t t_hi,
+                                                       const uint32_t* __restrict__ rk, GamAddr gam_of, uint32_t lmask,
+                                                       bool valid)
 {
     uint32_t has = 0;
     if (valid) {
@@ -427,7 +442,7 @@ __device__ __forceinline__ uint32_t geometric_gamma(const Img<SMEM>& img, uint32
                 const uint32_t w = (m & 3u) == 0 ? v.x : (m & 3u) == 1 ? v.y : (m & 3u) == 2 ? v.z : v.w;
                 k += 1 + geometric_skip(w, n, inv_lnq, [&](int g) { return img.ld32(geo + 4u * (uint32_t)g); });
                 if (k >= n) break;
-                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(gam + 4u * (uint32_t)k), "r"(lmask) : "memory");
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(gam_of((uint32_t)k)), "r"(lmask) : "memory");
             }
         }
     }

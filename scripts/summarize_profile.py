@@ -37,13 +37,15 @@ lpath = os.path.join(G, f"launches_{tag}.csv")
 if os.path.exists(lpath):
     rows = [r for r in csv.reader(open(lpath)) if len(r) > 10 and r[0] != "ID"]
     tot = sum(float(r[-1]) for r in rows)
-    k1 = sum(float(r[-1]) for r in rows if "traj_kernel" in r[4])
+    # share of the dominant trajectory kernel (K1b bitslice_kernel or K1 traj_kernel)
+    top = "bitslice_kernel" if any("bitslice_kernel" in r[4] for r in rows) else "traj_kernel"
+    k1 = sum(float(r[-1]) for r in rows if top in r[4])
     with open(os.path.join(P, f"launches_{tag}.csv"), "w") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "block", "grid", "gpu_time_ns"])
         for r in rows:
             w.writerow([r[4][:90], r[7], r[8], r[-1]])
-        w.writerow([f"# traj_kernel share of all launched GPU time: {k1 / tot:.6f}", "", "", ""])
+        w.writerow([f"# {top} share of all launched GPU time: {k1 / tot:.6f}", "", "", ""])
 
 rep = os.path.join(G, f"prof_{tag}.ncu-rep")
 if not os.path.exists(rep):
@@ -53,8 +55,10 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 get = {h: (u, v) for h, u, v in zip(hdr, units, vals)}
 out = io.StringIO()
-out.write(f"ncu --set full --clock-control none, one traj_kernel (K1) launch, tag {tag}\n")
-out.write(f"kernel: {get.get('Kernel Name', ('', '?'))[1]}\n\n")
+kname = get.get('Kernel Name', ('', '?'))[1]
+kshort = "K1b" if "bitslice" in kname else "K1"
+out.write(f"ncu --set full --clock-control none, one {kshort} launch, tag {tag}\n")
+out.write(f"kernel: {kname}\n\n")
 keys = ["gpu__time_duration.sum", "sm__cycles_active.avg", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active",
@@ -107,6 +111,6 @@ if len(srows) > 2:
     out.write("top opcodes (warp-instructions x 32 per node-update):\n")
     for k, v in c.most_common(28):
         out.write(f"  {k:26s} {v * 32 / nu if nu else v:8.2f}\n")
-with open(os.path.join(P, f"ncu_K1_{tag}.txt"), "w") as f:
+with open(os.path.join(P, f"ncu_{kshort}_{tag}.txt"), "w") as f:
     f.write(out.getvalue())
 print(out.getvalue())

@@ -197,3 +197,43 @@ def test_outside_shape_is_refused(pbn):
     with pytest.raises(Exception):
         gpu_run(pm, model, Predicate(np.array([5], np.uint16), np.array([1], np.uint8)), n_chains=40, steps=10,
                 layout=BS)
+
+
+# NEXT-2 in K1b: the geometric-skip stream (reading Q18; oracle pinned in
+# tests/test_oracle_geometric.py): one warp per step clears the gamma words
+# and draws gamma(t) by skips, every other step part as VECTOR
+@pytest.mark.parametrize("key,chains", [("C1", 4), ("C2", 200), ("C3", 64)])
+def test_geometric_all_chains(pbn, key, chains):
+    c = CONFIGS[key]
+    model, pred = config_model(key), config_predicate(key)
+    pm = pbn.pbn_load(model, geometric=True)
+    steps, burn_in = min(c.steps, 3000), min(c.burn_in, 500)
+    g = gpu_run(pm, model, pred, n_chains=chains, steps=steps, burn_in=burn_in, seed=c.sim_seed, batch=c.batch,
+                layout=BS)
+    assert pbn.pbn_last_kernel() == "K1b"
+    st, I, ws = oracle_run(model, pred, np.arange(chains), steps=steps, burn_in=burn_in, seed=c.sim_seed,
+                           batch=c.batch, geometric=True, threads=os.cpu_count() or 8)
+    packed = pack_states(st)
+    for j in range(chains):
+        compare_chain(g, j, packed[j], ws[j], steps, c.batch)
+    assert np.array_equal(g["totals"], ostats.totals(ws))
+
+
+def test_geometric_launch_shapes_equal_K1(pbn, monkeypatch):
+    """Warps, persistent chunks, a ragged group and the global image give K1's
+    outputs exactly under the geometric stream."""
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = pbn.pbn_load(model, geometric=True)
+    kw = dict(n_chains=2007, steps=400, burn_in=90, seed=6, batch=40)
+    ref = gpu_run(pm, model, pred, cluster_size=1, layout=1, schedule=1, **kw)
+    assert pbn.pbn_last_kernel() == "K1"
+    for extra in [dict(warps=1), dict(warps=9), dict(warps=0, schedule=2, chunk_steps=13),
+                  dict(warps=25, schedule=2, chunk_steps=1)]:
+        g = gpu_run(pm, model, pred, layout=BS, **kw, **extra)
+        for k in ALL:
+            assert np.array_equal(g[k], ref[k]), (extra, k)
+    monkeypatch.setenv("PBN_FORCE_GLOBAL_IMAGE", "1")
+    g = gpu_run(pm, model, pred, layout=BS, **kw)
+    assert pbn.pbn_last_kernel() == "K1b-global"
+    for k in ALL:
+        assert np.array_equal(g[k], ref[k]), ("global image", k)
