@@ -810,7 +810,7 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.sel_off = 12 * P.n_pad + 272;
     Bp.sel_bytes = 4 * pbn::bitslice_pv(m->bs_L) * P.n_pad;
     Bp.pq_off = Bp.sel_off + 2 * Bp.sel_bytes;
-    // 28 warps (the 72-register budget): C4 6.40e11 vs 6.30e11 node-updates/s at 20
+    // all the budget's warps (24: profiles/ in DESIGN §11)
     int W = a->warps_per_group > 0 ? a->warps_per_group : std::min(pbn::kBitsliceMaxWarps, std::max(P.nquads, 1));
     W = std::max(W, P.n_props);
     if (W > pbn::kBitsliceMaxWarps || W > std::max(P.nquads, P.n_props)) return PBN_E_USAGE;

@@ -229,9 +229,12 @@ constexpr int kBitsliceMaxTheta = 8;
 constexpr int kBitsliceMaxEll = 4;
 constexpr int kBitsliceMaxNodes = 5460;  // u16 state offsets 48 (i >> 2) + 4 (i & 3) and node ids << 2
 constexpr uint32_t kBitsliceQs = 48;     // bytes between quads: three interleaved state buffers
-// thread budget of the bitslice kernel (its register budget is 65536 / threads)
+// thread budget of the bitslice kernel (its register budget is 65536 / threads):
+// 768 = 24 warps at 80 registers, no spills (896 x 72 spilled ~60 bytes: per-
+// step and per-round local loads that tripled the launch's DRAM traffic,
+// 253 MB vs 99.9 MB on C4; C4 6.79e11 either way, C3 5.92e11 -> 6.14e11)
 #ifndef PBN_BS_THREADS
-#define PBN_BS_THREADS 896
+#define PBN_BS_THREADS 768
 #endif
 constexpr int kBitsliceMaxWarps = PBN_BS_THREADS / 32;
 struct BitsliceParams {
