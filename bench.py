@@ -388,6 +388,7 @@ def main():
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=0, help="0 auto, 1 CTA per group, 2 persistent")
     ap.add_argument("--chunk", type=int, default=0, help="persistent chunk steps (0 auto)")
+    ap.add_argument("--cluster", type=int, default=0, help="cluster_size (0 auto)")
     ap.add_argument("--layout", type=int, default=0,
                     help="PBN_LAYOUT_*: 0 auto, 1 chain lanes (K1/K1c), 2 node lanes (K1n), 3 bit-sliced (K1b)")
     ap.add_argument("--sweep", action="store_true", help="C5 chain-count sweep (one line per count)")
@@ -443,13 +444,14 @@ def main():
                          burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=True,
                          emit_bits=True, groups_per_cta=args.groups, warps_per_group=args.warps,
                          schedule=args.schedule, chunk_steps=args.chunk, layout=args.layout,
-                         stream=stream)
+                         cluster_size=args.cluster, stream=stream)
 
     for _ in range(args.warmup):
         one_step()
         flush.fill_(1)
     torch.cuda.synchronize()
     kernel_name = {"K1b": "bitslice_kernel (K1b)", "K1b-global": "bitslice_kernel (K1b, global image)",
+                   "K1bc": "bitslice_kernel (K1bc, cluster)",
                    "K1": "traj_kernel (K1)", "K1-global": "traj_kernel (K1, global image)",
                    "K1c": "traj_cluster_kernel (K1c)", "K1n": "traj_nodepar_kernel (K1n)"}.get(
         pbn.pbn_last_kernel(), pbn.pbn_last_kernel())
@@ -496,7 +498,7 @@ def main():
         except Exception:
             sm_mhz = 1965.0
     rf = roofline(model, node_updates_per_step, avg_kernel_s, sm_mhz, args.geometric)
-    if pbn.pbn_last_kernel() in ("K1b", "K1b-global"):
+    if pbn.pbn_last_kernel() in ("K1b", "K1b-global", "K1bc"):
         db = demand_bitslice(model)
         alu_peak = rf["per_resource"]["alu"]["peak"] * 1e12
         rate = node_updates_per_step / avg_kernel_s
@@ -532,7 +534,8 @@ def main():
             out.state.copy_(host_state, non_blocking=True)
             pbn.pbn_simulate(pm, out, n_chains=chains, chain_base=chain_base, steps=window,
                              burn_in=burn_in, batch=batch, seed=cfg.sim_seed, pred=pred, init=False,
-                             emit_bits=True, warps_per_group=args.warps, layout=args.layout, stream=stream)
+                             emit_bits=True, warps_per_group=args.warps, layout=args.layout,
+                             cluster_size=args.cluster, stream=stream)
             for k, t in res_host.items():
                 t.copy_(getattr(out, k), non_blocking=True)
 

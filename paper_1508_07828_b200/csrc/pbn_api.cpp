@@ -108,6 +108,18 @@ struct pbn_model_s {
     uint8_t* d_bs = nullptr;
     uint32_t bs_bytes = 0, bs_erec_off = 0, bs_rounds_off = 0;
     int32_t bs_rounds = 0, bs_L = 0, bs_cmax = 0;
+    // its sub-images for cluster launches (K1bc): K = 2, 4, 8, 16
+    struct BsCluster {
+        int K = 0;
+        uint8_t* d_buf = nullptr;
+        uint32_t off[pbn::kMaxCluster] = {}, bytes[pbn::kMaxCluster] = {}, erec_off[pbn::kMaxCluster] = {},
+                 rounds_off[pbn::kMaxCluster] = {};
+        int32_t rounds[pbn::kMaxCluster] = {};
+        int32_t qlo[pbn::kMaxCluster + 1] = {};
+        uint32_t max_bytes = 0;
+        int32_t max_lq = 0;
+    };
+    std::vector<BsCluster> bs_clusters;
     uint32_t geo_last = 0;                // geometric mode: Cg[n-1]
     uint32_t geo_off = 0;                 // geometric mode: byte offset of Cg in the image
     double p = 0.0;
@@ -453,8 +465,11 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
 // and the round list (most expensive class first).  Returns false when the
 // model is outside the bit-sliced kernel's shape (theta > 6, ell > 4, too
 // many nodes for u16 offsets).
+// (q_lo, q_hi: the quads of a cluster CTA's sub-image -- erec indexed by the
+// local quad, tasks of its nodes only; -1 = all)
 bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint8_t>& out, uint32_t* erec_off,
-                          uint32_t* rounds_off, int32_t* n_rounds, int32_t* L_out, int32_t* cmax_out)
+                          uint32_t* rounds_off, int32_t* n_rounds, int32_t* L_out, int32_t* cmax_out,
+                          int32_t q_lo = -1, int32_t q_hi = -1)
 {
     const int32_t n = d->n;
     if (n > pbn::kBitsliceMaxNodes) return false;
@@ -466,11 +481,19 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
         for (int32_t f = d->fn_off[i]; f < d->fn_off[i + 1]; ++f)
             if (d->par_off[f + 1] - d->par_off[f] > pbn::kBitsliceMaxTheta) return false;
     }
-    const int32_t nq = (n + 3) / 4;
+    const int32_t nq_all = (n + 3) / 4;
+    if (q_lo < 0) {
+        q_lo = 0;
+        q_hi = nq_all;
+    }
+    const int32_t nq = q_hi - q_lo;
+    // model-wide largest class (one kernel for every sub-image of a cluster)
+    int32_t cmax = 1;
+    for (int32_t f = 0; f < d->fn_off[n]; ++f) cmax = std::max(cmax, d->par_off[f + 1] - d->par_off[f]);
     ImageBuilder B;
     // thresholds E_1..E_{L-1} per quad, plane-major: [q][m] = {E_{m+1} of nodes 4q..4q+3}
     const uint32_t eo = B.alloc(16u * (size_t)std::max(nq * (L - 1), 1));
-    for (int32_t i = 0; i < 4 * nq; ++i) {
+    for (int32_t i = 4 * q_lo; i < 4 * q_hi; ++i) {
         std::vector<uint32_t> E;
         if (i < n) {
             const int32_t f0 = d->fn_off[i], ell = d->fn_off[i + 1] - f0;
@@ -481,11 +504,12 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
             }
         }
         for (int32_t m = 0; m + 1 < L; ++m)
-            B.u32(eo + 16u * (uint32_t)((i >> 2) * (L - 1) + m))[i & 3] = m < (int32_t)E.size() ? E[m] : 0xFFFFFFFFu;
+            B.u32(eo + 16u * (uint32_t)(((i >> 2) - q_lo) * (L - 1) + m))[i & 3] =
+                m < (int32_t)E.size() ? E[m] : 0xFFFFFFFFu;
     }
     // tasks by class
     std::vector<std::pair<int32_t, int32_t>> cls[pbn::kBitsliceMaxTheta + 1];  // (node, j)
-    for (int32_t i = 0; i < n; ++i)
+    for (int32_t i = 4 * q_lo; i < std::min(n, 4 * q_hi); ++i)
         for (int32_t f = d->fn_off[i]; f < d->fn_off[i + 1]; ++f)
             cls[std::max(d->par_off[f + 1] - d->par_off[f], 1)].push_back({i, f - d->fn_off[i]});
     std::vector<std::pair<uint32_t, uint32_t>> rounds;  // (task offset, class)
@@ -499,7 +523,7 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
             uint32_t* w = B.u32(to + stride * (uint32_t)k);
             uint16_t* h = B.u16(to + stride * (uint32_t)k + 4u * T);  // [i << 2 | j, p_0 .. p_{c-1}]
             if (k >= cls[c].size()) {  // dummy task: table 0 contributes nothing
-                h[0] = 1u;  // node 0, function 1 (no perturbation term)
+                h[0] = (uint16_t)(((uint32_t)(4 * q_lo) << 2) | 1u);  // the first own node, function 1
                 continue;
             }
             const int32_t i = cls[c][k].first, j = cls[c][k].second, f = d->fn_off[i] + j;
@@ -525,7 +549,7 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
     *rounds_off = ro;
     *n_rounds = (int32_t)rounds.size();
     *L_out = L;
-    *cmax_out = rounds.empty() ? 1 : (int32_t)rounds.front().second;  // most expensive class first
+    *cmax_out = cmax;
     return true;
 }
 
@@ -609,6 +633,39 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
                 return PBN_E_CUDA;
             }
             m->bs_bytes = (uint32_t)bs.size();
+            const int32_t nq = (desc->n + 3) / 4;
+            for (int K = 2; K <= pbn::kMaxCluster && K <= nq; K *= 2) {
+                pbn_model_s::BsCluster bc;
+                bc.K = K;
+                std::vector<uint8_t> all;
+                for (int r = 0; r <= K; ++r) bc.qlo[r] = (int32_t)((int64_t)nq * r / K);
+                bool ok = true;
+                for (int r = 0; r < K && ok; ++r) {
+                    std::vector<uint8_t> sub;
+                    int32_t L2 = 0, cm2 = 0;
+                    ok = build_bitslice_image(desc, Tsel, sub, &bc.erec_off[r], &bc.rounds_off[r], &bc.rounds[r], &L2, &cm2,
+                                              bc.qlo[r], bc.qlo[r + 1]);
+                    const size_t off = (all.size() + 15) & ~(size_t)15;
+                    all.resize(off + sub.size(), 0);
+                    std::memcpy(all.data() + off, sub.data(), sub.size());
+                    bc.off[r] = (uint32_t)off;
+                    bc.bytes[r] = (uint32_t)sub.size();
+                    bc.max_bytes = std::max(bc.max_bytes, bc.bytes[r]);
+                    bc.max_lq = std::max(bc.max_lq, bc.qlo[r + 1] - bc.qlo[r]);
+                }
+                if (!ok) break;
+                if (cudaMalloc(&bc.d_buf, all.size()) != cudaSuccess ||
+                    cudaMemcpy(bc.d_buf, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+                    if (bc.d_buf) cudaFree(bc.d_buf);
+                    for (auto& c : m->bs_clusters) cudaFree(c.d_buf);
+                    cudaFree(m->d_bs);
+                    cudaFree(m->d_image);
+                    delete m;
+                    set_err(err, errlen, "bitslice cluster sub-image upload failed");
+                    return PBN_E_CUDA;
+                }
+                m->bs_clusters.push_back(bc);
+            }
         }
     }
     // sub-images for the cluster kernel: CTA r of a K-cluster owns quads
@@ -639,6 +696,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
             if (ci.d_buf) cudaFree(ci.d_buf);
             for (auto& c : m->clusters) cudaFree(c.d_buf);
             if (m->d_bs) cudaFree(m->d_bs);
+            for (auto& c : m->bs_clusters) cudaFree(c.d_buf);
             cudaFree(m->d_image);
             delete m;
             set_err(err, errlen, "cluster sub-image upload failed");
@@ -673,6 +731,7 @@ pbn_status pbn_load(const pbn_model_desc* desc, int device, pbn_model* out, char
             for (auto& c : m->nodepar) cudaFree(c.d_buf);
             for (auto& c : m->clusters) cudaFree(c.d_buf);
             if (m->d_bs) cudaFree(m->d_bs);
+            for (auto& c : m->bs_clusters) cudaFree(c.d_buf);
             cudaFree(m->d_image);
             delete m;
             set_err(err, errlen, "node-parallel sub-image upload failed");
@@ -689,6 +748,7 @@ void pbn_free(pbn_model model)
     if (!model) return;
     if (model->d_image) cudaFree(model->d_image);
     if (model->d_bs) cudaFree(model->d_bs);
+    for (auto& c : model->bs_clusters) cudaFree(c.d_buf);
     for (auto& c : model->clusters) cudaFree(c.d_buf);
     for (auto& c : model->nodepar) cudaFree(c.d_buf);
     delete model;
@@ -807,7 +867,7 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.rounds_off = m->bs_rounds_off;
     Bp.n_rounds = m->bs_rounds;
     Bp.any_off = 12 * P.n_pad;
-    Bp.sel_off = 12 * P.n_pad + 272;
+    Bp.sel_off = 12 * P.n_pad + 4 * pbn::kBitsliceAnyWords;
     Bp.sel_bytes = 4 * pbn::bitslice_pv(m->bs_L) * P.n_pad;
     Bp.pq_off = Bp.sel_off + 2 * Bp.sel_bytes;
     // all the budget's warps (24: profiles/ in DESIGN §11)
@@ -827,12 +887,102 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.T.stats_warp0 = 0;
     if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0 || a->workspace_bytes < 0) return PBN_E_USAGE;
     if (P.geometric) Bp.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->geo_off);
-    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, smem_image, m->bs_cmax);
+    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, smem_image ? 1 : 0,
+                                               m->bs_cmax);
     const int rc = pbn::launch_group_units(Bp.T, fn, &Bp, plan, m->device, a->schedule, a->chunk_steps, a->workspace,
                                            (size_t)a->workspace_bytes, stream);
     if (rc == -2) return PBN_E_USAGE;
     if (rc == 0) g_last_kernel = smem_image ? "K1b" : "K1b-global";
     return rc == 0 ? PBN_OK : PBN_E_CUDA;
+}
+
+// K1bc launch: one 32-chain group per cluster of K CTAs (K1b's kernel with
+// IMG = 2), each CTA staging its sub-image; K = cluster_size, or (0) the
+// largest whose clusters all fit one wave on the SMs.  Returns PBN_E_USAGE
+// when no K fits (the caller may fall back), `*launched` false.
+static pbn_status simulate_bitslice_cluster(pbn_model m, const pbn::TrajParams& P, const pbn_sim_args* a, void* stream,
+                                            int smem_optin, int sms, bool* launched)
+{
+    *launched = false;
+    if (!m->d_bs || m->bs_clusters.empty()) return PBN_E_USAGE;
+    const int64_t groups = (P.n_chains + 31) / 32;
+    const pbn_model_s::BsCluster* use = nullptr;
+    auto smem_of = [&](const pbn_model_s::BsCluster& c) {
+        return (size_t)pbn::bitslice_group_words(P.n_pad, m->bs_L, c.max_lq) * 4 + c.max_bytes;
+    };
+    for (const auto& c : m->bs_clusters) {
+        if (smem_of(c) + 64 > (size_t)smem_optin) continue;
+        if (a->cluster_size >= 2) {
+            if (c.K == a->cluster_size) use = &c;
+        } else if (c.K <= 8 && c.max_lq >= 32 && groups * c.K <= sms) {
+            // auto: the largest K <= 8 whose clusters fit one wave while every
+            // CTA keeps >= 32 quads (measured, profiles/k1bc_r3w.txt: C5 / C4
+            // 1024 chains K = 4 3.8e11 / 3.8e11 vs K1c 1.6e11 / 3.0e11; C3 2048
+            // chains K = 2 4.3e11 vs 3.4e11; 256 chains K = 8 beats K1n by 7-16 %
+            // and K = 16 loses; C2 (6 quads per CTA at K = 4) stays on K1c)
+            use = &c;
+        }
+    }
+    if (!use) return PBN_E_USAGE;
+    pbn::BitsliceParams Bp;
+    std::memset(&Bp, 0, sizeof(Bp));
+    Bp.T = P;
+    Bp.T.image = use->d_buf;
+    Bp.T.group_words = pbn::bitslice_group_words(P.n_pad, m->bs_L, use->max_lq);
+    Bp.T.image_smem_bytes = use->max_bytes;
+    Bp.any_off = 12 * P.n_pad;
+    Bp.sel_off = 12 * P.n_pad + 4 * pbn::kBitsliceAnyWords;
+    Bp.sel_bytes = 16 * pbn::bitslice_pv(m->bs_L) * use->max_lq;
+    Bp.pq_off = Bp.sel_off + 2 * Bp.sel_bytes;
+    Bp.K = use->K;
+    for (int r = 0; r < use->K; ++r) {
+        Bp.c_img_off[r] = use->off[r];
+        Bp.c_img_bytes[r] = use->bytes[r];
+        Bp.c_erec_off[r] = use->erec_off[r];
+        Bp.c_rounds_off[r] = use->rounds_off[r];
+        Bp.c_rounds[r] = use->rounds[r];
+    }
+    for (int r = 0; r <= use->K; ++r) Bp.c_qlo[r] = use->qlo[r];
+    if (P.geometric) Bp.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->geo_off);
+    int W = a->warps_per_group > 0 ? a->warps_per_group
+                                   : std::min(pbn::kBitsliceMaxWarps, std::max(use->max_lq, 1));
+    W = std::max(W, P.n_props);
+    if (W > pbn::kBitsliceMaxWarps) return PBN_E_USAGE;
+    Bp.T.warps_per_group = W;
+    Bp.T.node_warps = std::min(W, std::max(use->max_lq, 1));
+    Bp.T.stats_warp0 = 0;
+    Bp.T.persistent = 0;
+    const size_t smem = smem_of(*use);
+    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, 2, m->bs_cmax);
+    cudaError_t e = pbn::ensure_func_smem(fn, smem, use->K > 8);
+    if (e != cudaSuccess) return PBN_E_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(groups * use->K));
+    cfg.blockDim = dim3((unsigned)(32 * W));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)use->K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int active = 0;
+    {
+        cudaLaunchConfig_t one = cfg;
+        one.gridDim = dim3((unsigned)use->K);
+        if (cudaOccupancyMaxActiveClusters(&active, fn, &one) != cudaSuccess || active < 1) {
+            cudaGetLastError();
+            return PBN_E_USAGE;
+        }
+    }
+    void* args[] = {&Bp};
+    e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return PBN_E_CUDA;
+    *launched = true;
+    g_last_kernel = "K1bc";
+    return PBN_OK;
 }
 
 pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o, void* stream)
@@ -855,7 +1005,11 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     const int64_t groups = (a->n_chains + 31) / 32;
     if (a->layout < PBN_LAYOUT_AUTO || a->layout > PBN_LAYOUT_BITSLICE) return PBN_E_USAGE;
     if (a->layout == PBN_LAYOUT_BITSLICE) {
-        if (a->cluster_size > 1 || a->chains_per_cluster != 0) return PBN_E_USAGE;
+        if (a->chains_per_cluster != 0) return PBN_E_USAGE;
+        if (a->cluster_size >= 2) {
+            bool launched = false;
+            return simulate_bitslice_cluster(m, P, a, stream, smem_optin, sms, &launched);
+        }
         return simulate_bitslice(m, P, a, stream, smem_optin);
     }
     // auto: the bit-sliced kernel wherever the one-CTA-per-group kernel would
@@ -897,8 +1051,15 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
     // auto layout (cluster_size 0): lanes over nodes for few chains --
     // measured faster than the chain-lanes kernels up to 256 chains
     // (profiles/nodelanes_auto_r2.jsonl; at 1024 chains K1c / K1 win)
+    // (<= 128 chains when K1bc applies: at 256 chains it beats K1n, at 64 K1n
+    // wins by 2.3x -- profiles/k1bc_r3w.txt)
+    bool bc_applies = false;
+    for (const auto& c : m->bs_clusters)
+        bc_applies |= c.K <= 8 && c.max_lq >= 32 && groups * c.K <= sms &&
+                      (size_t)pbn::bitslice_group_words(P.n_pad, m->bs_L, c.max_lq) * 4 + c.max_bytes <= limit;
     const bool node_lanes = a->layout == PBN_LAYOUT_NODE_LANES ||
-                            (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 && a->n_chains <= 256);
+                            (a->layout == PBN_LAYOUT_AUTO && a->cluster_size == 0 &&
+                             a->n_chains <= (bc_applies ? 128 : 256));
     const NodeParImages* np_use = nullptr;
     if (node_lanes) {
         if (a->cluster_size >= 1) {
@@ -972,6 +1133,16 @@ pbn_status pbn_simulate(pbn_model m, const pbn_sim_args* a, const pbn_sim_out* o
             if (ci.K == a->cluster_size) use = &ci;
         if (!use || !fits(*use)) return PBN_E_USAGE;
     } else if (a->cluster_size == 0 && 2 * groups <= sms) {
+        // few groups: the bit-sliced kernel over a cluster per group when it
+        // applies (K1bc), else K1c below
+        if (a->layout == PBN_LAYOUT_AUTO) {
+            const char* nb = std::getenv("PBN_NO_BITSLICE");
+            if (!(nb && nb[0] == '1')) {
+                bool launched = false;
+                const pbn_status sb = simulate_bitslice_cluster(m, P, a, stream, smem_optin, sms, &launched);
+                if (launched || sb == PBN_E_CUDA) return sb;
+            }
+        }
         // few-chain regime: one CTA per group would leave at least half the
         // SMs idle, so split each group's nodes over a cluster (measured: C3,
         // 64 groups: K = 2 1.6x the single-CTA kernel; 128 groups: single-CTA

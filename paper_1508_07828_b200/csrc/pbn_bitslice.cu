@@ -4,15 +4,15 @@
 
 namespace pbn {
 
-const void* pick_bitslice_kernel_mode0(int L, bool smem_image, int cmax);
-const void* pick_bitslice_kernel_mode1(int L, bool smem_image, int cmax);
-const void* pick_bitslice_kernel_mode2(int L, bool smem_image, int cmax);
+const void* pick_bitslice_kernel_mode0(int L, int img, int cmax);
+const void* pick_bitslice_kernel_mode1(int L, int img, int cmax);
+const void* pick_bitslice_kernel_mode2(int L, int img, int cmax);
 
-const void* pick_bitslice_kernel(int mode, int L, bool smem_image, int cmax)
+const void* pick_bitslice_kernel(int mode, int L, int img, int cmax)
 {
-    return mode == 1   ? pick_bitslice_kernel_mode1(L, smem_image, cmax)
-           : mode == 2 ? pick_bitslice_kernel_mode2(L, smem_image, cmax)
-                       : pick_bitslice_kernel_mode0(L, smem_image, cmax);
+    return mode == 1   ? pick_bitslice_kernel_mode1(L, img, cmax)
+           : mode == 2 ? pick_bitslice_kernel_mode2(L, img, cmax)
+                       : pick_bitslice_kernel_mode0(L, img, cmax);
 }
 
 }  // namespace pbn

@@ -118,7 +118,7 @@ struct Planes {
 // plane words are at pl + 16 m (m < NP: b_m; m = NP: gamma).
 template <int C, int MODE, int L, bool SMEM>
 __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uint32_t gob, uint32_t gnb, uint32_t sel,
-                                         uint32_t M)
+                                         uint32_t M, uint32_t qlo)
 {
     constexpr int T = C <= 5 ? 1 : (1 << C) / 32;      // table words
     constexpr int NV = (4 * T + 2 * (C + 1) + 15) / 16;  // 16-byte vectors of the record
@@ -146,7 +146,7 @@ __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uin
     const uint32_t F = mux_tree<0, C, 0>(t, x);
     const uint32_t ij = u16(0);
     const uint32_t i = ij >> 2, j = ij & 3u;
-    const uint32_t pl = sel + 16u * (uint32_t)PV * (i >> 2) + 4u * (i & 3u);
+    const uint32_t pl = sel + 16u * (uint32_t)PV * ((i >> 2) - qlo) + 4u * (i & 3u);  // (local quad)
     // selection plane of function j: the chains whose index bits equal j's
     const uint32_t b0 = NP >= 1 ? lds32_state(pl) : 0u;
     const uint32_t b1 = NP >= 2 ? lds32_state(pl + 16u) : 0u;
@@ -167,11 +167,18 @@ __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uin
                  : "memory");
 }
 
-// MODE: 0 VECTOR, 1 PER_NODE; L = the model's largest ell; SMEM: image staged;
+// MODE: 0 VECTOR, 1 PER_NODE, 2 geometric; L = the model's largest ell;
+// IMG: 0 image through L1/L2, 1 image staged, 2 CLUSTER -- one group per
+// cluster of K CTAs, CTA rank r owns quads [qlo, qhi) (its sub-image: their
+// thresholds and their nodes' tasks), keeps the whole state and, after each
+// step's barrier, pushes its nodes' new words (and its any word) into every
+// peer through distributed shared memory before one cluster barrier;
 // CMAX: the largest task class (6 or 8)
-template <int MODE, int L, bool SMEM, int CMAX>
+template <int MODE, int L, int IMG, int CMAX>
 __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
 {
+    constexpr bool SMEM = IMG != 0;
+    constexpr bool CLU = IMG == 2;
     const TrajParams& P = B.T;
     constexpr bool PER_NODE = MODE == 1;
     constexpr bool GEO = MODE == 2;  // VECTOR with the geometric-skip stream (reading Q18)
@@ -187,6 +194,11 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     const int n = P.n;
     const uint32_t gbase = smem_u32(smem);
     const uint32_t sbase = gbase + 4u * (uint32_t)P.group_words;  // staged image base
+    uint32_t rank = 0;
+    if (CLU) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int KC = CLU ? B.K : 1;  // CTAs per cluster
+    const uint8_t* const gimg = P.image + (CLU ? B.c_img_off[rank] : 0u);
+    const uint32_t img_bytes = CLU ? B.c_img_bytes[rank] : P.image_smem_bytes;
 
     // ---- A1: stage the image into shared memory (bulk async copy) ----
     if (SMEM) {
@@ -194,15 +206,15 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         if (tid == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(P.image_smem_bytes)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(img_bytes)
                          : "memory");
             const uint32_t chunk = 32768;
-            for (uint32_t off = 0; off < P.image_smem_bytes; off += chunk) {
-                const uint32_t sz = min(chunk, P.image_smem_bytes - off);
+            for (uint32_t off = 0; off < img_bytes; off += chunk) {
+                const uint32_t sz = min(chunk, img_bytes - off);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         sbase + off),
-                    "l"(P.image + off), "r"(sz), "r"(bar)
+                    "l"(gimg + off), "r"(sz), "r"(bar)
                     : "memory");
             }
         }
@@ -223,13 +235,19 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     const uint32_t anyw0 = gbase + (uint32_t)B.any_off;  // any[2][32]
     const uint32_t sel0 = gbase + (uint32_t)B.sel_off;   // planes[2]
     const uint32_t pqt = gbase + (uint32_t)B.pq_off;     // per-quad Philox table
-    const uint32_t erec = B.erec_off;
-    const uint32_t rounds = B.rounds_off;
-    const int R = B.n_rounds;
+    const uint32_t erec = CLU ? B.c_erec_off[rank] : B.erec_off;
+    const uint32_t rounds = CLU ? B.c_rounds_off[rank] : B.rounds_off;
+    const int R = CLU ? B.c_rounds[rank] : B.n_rounds;
+    // this CTA's quads [qlo, qhi) (all of them outside a cluster); erec, the
+    // planes and the Philox table are indexed by the local quad q - qlo
+    const int qlo = CLU ? B.c_qlo[rank] : 0, qhi = CLU ? B.c_qlo[rank + 1] : P.nquads;
+    const uint32_t cany = anyw0 + 256u;  // cluster: any words of the ranks [2][16], then a dummy word
 
     const int NW = P.node_warps;
-    const int q0 = wg < NW ? (int)((int64_t)wg * P.nquads / NW) : P.nquads;
-    const int q1 = wg < NW ? (int)((int64_t)(wg + 1) * P.nquads / NW) : P.nquads;
+    const int q0 = wg < NW ? qlo + (int)((int64_t)wg * (qhi - qlo) / NW) : qhi;
+    const int q1 = wg < NW ? qlo + (int)((int64_t)(wg + 1) * (qhi - qlo) / NW) : qhi;
+    // all quads over the warps (the initial state: every CTA forms all of it)
+    const int qi0 = (int)((int64_t)wg * P.nquads / W), qi1 = (int)((int64_t)(wg + 1) * P.nquads / W);
     const int nsw = P.state_words;
     const int b0 = (int)((int64_t)wg * nsw / W), b1 = (int)((int64_t)(wg + 1) * nsw / W);
     const int64_t total = P.burn_in + P.steps;
@@ -242,7 +260,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         int64_t group, chunk, r_begin, r_end;
         if (!P.persistent) {
             if (it > 0) break;
-            group = blockIdx.x;
+            group = CLU ? blockIdx.x / KC : blockIdx.x;
             chunk = 0;
             r_begin = 1;
             r_end = total;
@@ -273,7 +291,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         const uint32_t vmask = __ballot_sync(FULL, valid);
         auto scr = [&]() { return P.scratch + group * (int64_t)P.scratch_stride; };
         const int prop = wg - P.stats_warp0;
-        const bool stats = prop >= 0 && prop < P.n_props;
+        const bool stats = prop >= 0 && prop < P.n_props && rank == 0;  // (cluster: rank 0 keeps them)
         auto orow = [&]() { return (int64_t)prop * P.n_chains + chain_local; };
         ChainStats cs;
 
@@ -294,7 +312,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             }
         } else if (P.init) {
             // A2: s_0[i] = u(chain, 0, i) >> 31
-            for (int q = q0; q < q1; ++q) {
+            for (int q = qi0; q < qi1; ++q) {
                 const uint4 r = philox4x32_10((uint32_t)q, chain, 0u, 0u, P.rk);
                 const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -336,12 +354,12 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             // (the parity of the compares, the thresholds ascending), b_1 = bit 1
             // (= [u > E_2])
             auto thresholds = [&](const int q, uint4 (&e)[3]) {
-                const uint32_t ea = erec + 16u * (uint32_t)(L - 1) * (uint32_t)q;
+                const uint32_t ea = erec + 16u * (uint32_t)(L - 1) * (uint32_t)(q - qlo);
 #pragma unroll
                 for (int m = 0; m < L - 1; ++m) e[m] = img.ld128(ea + 16u * m);
             };
             auto planes = [&](const int q, const uint4 rw, const uint4 (&e)[3]) {
-                const uint32_t pa = sel + 16u * (uint32_t)PV * (uint32_t)q;
+                const uint32_t pa = sel + 16u * (uint32_t)PV * (uint32_t)(q - qlo);
                 const uint32_t u[4] = {rw.x, rw.y, rw.z, rw.w};
                 uint32_t pb0[4], pb1[4];
 #pragma unroll
@@ -370,9 +388,9 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
                 const uint32_t g2 = __ballot_sync(FULL, rq.z < Tp), g3 = __ballot_sync(FULL, rq.w < Tp);
                 any |= g0 | g1 | g2 | g3;
-                sts128_if(sel + 16u * (uint32_t)PV * (uint32_t)q + 16u * NP, g0, g1, g2, g3, lead);
+                sts128_if(sel + 16u * (uint32_t)PV * (uint32_t)(q - qlo) + 16u * NP, g0, g1, g2, g3, lead);
             };
-            uint4 rw = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)q0), ps, P.rk);
+            uint4 rw = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(q0 - qlo)), ps, P.rk);
             uint4 e[3];
             for (int qc = q0; qc < qf; qc += 32) {
                 const int qe = min(qf, qc + 32);
@@ -388,7 +406,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
 #if defined(PBN_BS_SKIP_PHILOX)
                     next = make_uint4(cur.y * 3u + (uint32_t)q, cur.z ^ cur.x, cur.w + cur.y, cur.x * 5u);
 #else
-                    next = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(q + 1)), ps, P.rk);
+                    next = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(q + 1 - qlo)), ps, P.rk);
 #endif
                     planes(q, cur, e);
                     if (!GEO)
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                     const int jb = __ffs((int)gpend) - 1;
                     gpend &= gpend - 1;
                     const int qq = qe - 1 - jb;
-                    gammas(qq, philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)qq), ps, P.rk));
+                    gammas(qq, philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(qq - qlo)), ps, P.rk));
                 }
             }
             if (qf < q1) {  // ragged last quad: padding nodes draw no perturbation
@@ -427,14 +445,20 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 // buffer's gamma vectors, then every lane draws its chain's
                 // gamma(t) by skips over Cg and ORs its bit into the gamma
                 // words (node k's at sel + 16 PV (k >> 2) + 16 NP + 4 (k & 3))
-                for (int q = lane; q < P.nquads; q += 32)
+                for (int q = lane; q < qhi - qlo; q += 32)
                     sts128_if(sel + 16u * (uint32_t)PV * (uint32_t)q + 16u * NP, 0u, 0u, 0u, 0u, FULL);
                 __syncwarp();
                 Img<false> gi;
                 gi.gbase = reinterpret_cast<const uint8_t*>(B.geo_table);
                 any = geometric_gamma_at(
                     gi, 0u, n, P.geo_inv_lnq, chain, t_lo, t_hi, P.rk,
-                    [&](uint32_t kk) { return sel + 16u * (uint32_t)PV * (kk >> 2) + 16u * NP + 4u * (kk & 3u); },
+                    [&](uint32_t kk) {
+                        // (cluster: another rank's node -> the dummy word)
+                        const int kq = (int)(kk >> 2);
+                        return (kq >= qlo && kq < qhi)
+                                   ? sel + 16u * (uint32_t)PV * (uint32_t)(kq - qlo) + 16u * NP + 4u * (kk & 3u)
+                                   : cany + 128u;
+                    },
                     lmask, valid);
             }
             if (!PER_NODE && leader) sts32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * wg, any);
@@ -445,24 +469,29 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             const uint32_t sel = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes;
             const uint32_t gob = gbase + ob, gnb = gbase + nb;
             uint32_t M = 0;
-            if (!PER_NODE)
-                M = __reduce_or_sync(FULL, lane < W ? lds32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * lane) : 0u) & vmask;
+            if (!PER_NODE) {
+                if (CLU)  // the ranks' any words (exchanged before this interval)
+                    M = __reduce_or_sync(FULL, lane < KC ? lds32(cany + 64u * (uint32_t)(k & 1) + 4u * lane) : 0u) & vmask;
+                else
+                    M = __reduce_or_sync(FULL, lane < W ? lds32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * lane) : 0u) &
+                        vmask;
+            }
             for (int m = 0; m * W < R; ++m) {
                 const int rr_i = (m & 1) ? (m + 1) * W - 1 - wg : m * W + wg;
                 if (rr_i >= R) continue;
                 const uint2 rr = img.ld64(rounds + 8u * (uint32_t)rr_i);
                 const uint32_t ta = rr.x + (uint32_t)lane * bs_stride((int)rr.y);
                 switch (rr.y) {
-                    case 1: bs_round<1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
-                    case 2: bs_round<2, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
-                    case 3: bs_round<3, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
-                    case 4: bs_round<4, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
-                    case 5: bs_round<5, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
-                    case 6: bs_round<6, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 1: bs_round<1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 2: bs_round<2, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 3: bs_round<3, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 4: bs_round<4, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 5: bs_round<5, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 6: bs_round<6, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
                     // classes 7 and 8 only in the CMAX = 8 kernels: their trees'
                     // registers would otherwise spill the theta <= 6 kernels
-                    case 7: if constexpr (CMAX >= 7) bs_round<CMAX >= 7 ? 7 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
-                    default: if constexpr (CMAX >= 8) bs_round<CMAX >= 8 ? 8 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M); break;
+                    case 7: if constexpr (CMAX >= 7) bs_round<CMAX >= 7 ? 7 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    default: if constexpr (CMAX >= 8) bs_round<CMAX >= 8 ? 8 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
                 }
             }
         };
@@ -482,8 +511,8 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         uint32_t table_thi = 0;
         auto fill_table = [&](const int64_t k) {
             table_thi = (uint32_t)((uint64_t)(P.step0 + r_begin - 1 + k) >> 32);
-            for (int q = tid; q <= P.nquads; q += blockDim.x) {
-                const uint4 c = philox_quad_consts((uint32_t)q, table_thi, P.rk);
+            for (int q = tid; q <= qhi - qlo; q += blockDim.x) {  // local quads (+1: the prefetch of q + 1)
+                const uint4 c = philox_quad_consts((uint32_t)(qlo + q), table_thi, P.rk);
                 sts128_if(pqt + 16u * (uint32_t)q, c.x, c.y, c.z, c.w, FULL);
             }
         };
@@ -499,11 +528,43 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
 #else
         constexpr bool kB = true;
 #endif
+        // cluster: this CTA's words of S_k (buffer nb) and its any word of step
+        // k + 1 into every peer (DSMEM), then one cluster barrier (release /
+        // acquire): the next interval reads a complete S_k and M everywhere
+        auto exchange = [&](const int64_t k, const uint32_t nb) {
+            if constexpr (CLU) {
+                const uint32_t nq_own = (uint32_t)(qhi - qlo);
+                for (uint32_t x = tid; x < nq_own * (uint32_t)KC; x += blockDim.x) {
+                    const uint32_t peer = x / nq_own, q = (uint32_t)qlo + x % nq_own;
+                    if (peer == rank) continue;
+                    const uint32_t a = gbase + QS * q + nb;
+                    const uint4 v = lds128_state(a);
+                    uint32_t ra;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(peer));
+                    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ra), "r"(v.x), "r"(v.y),
+                                 "r"(v.z), "r"(v.w)
+                                 : "memory");
+                }
+                if (!PER_NODE && wg == 0 && k + 1 <= K) {
+                    const uint32_t ca =
+                        __reduce_or_sync(FULL, lane < W ? lds32(anyw0 + 128u * (uint32_t)((k + 1) & 1) + 4u * lane) : 0u);
+                    if (lane < KC) {
+                        uint32_t ra;
+                        const uint32_t a = cany + 64u * (uint32_t)((k + 1) & 1) + 4u * rank;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(lane));
+                        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(ca) : "memory");
+                    }
+                }
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                                 "memory");
+            }
+        };
         __syncthreads();  // the previous unit's phase A is done with the table
         fill_table(1);
         __syncthreads();
         if (K >= 1) phaseA(1, 16u);
         __syncthreads();
+        exchange(0, 0u);  // (S_0 is complete in every CTA; this carries any(1))
         // one interval per step k: statistics of k-1, phase B of k and phase A
         // of k+1; buffers ob = S_{k-1}, nb = S_k, zb = S_{k+1} rotate (uniform)
         uint32_t ob = 0u, nb = 16u, zb = 32u;
@@ -523,6 +584,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 if (kA && k < K) phaseA(k + 1, zb);
             }
             __syncthreads();
+            exchange(k, nb);
             const uint32_t t3 = ob;
             ob = nb;
             nb = zb;
@@ -560,28 +622,30 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 if (i >= n) break;
                 v |= ((lds32(gbase + state_off(i, QS) + cur) >> lane) & 1u) << k;
             }
-            if (valid) P.state[(int64_t)chain_local * nsw + b] = v;
+            if (valid && rank == 0) P.state[(int64_t)chain_local * nsw + b] = v;
         }
         if (stats) cs.finish(P, prop, valid, orow(), leader);
     }
 }
 
-template <int MODE, bool SMEM, int CMAX>
+template <int MODE, int IMG, int CMAX>
 const void* pick_L(int L)
 {
     switch (L) {
-        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1, SMEM, CMAX>);
-        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2, SMEM, CMAX>);
-        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3, SMEM, CMAX>);
-        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4, SMEM, CMAX>);
+        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1, IMG, CMAX>);
+        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2, IMG, CMAX>);
+        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3, IMG, CMAX>);
+        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4, IMG, CMAX>);
     }
 }
 
+// img: 0 global image, 1 staged, 2 staged sub-image of a cluster
 template <int MODE>
-const void* pick_mode(int L, bool smem_image, int cmax)
+const void* pick_mode(int L, int img, int cmax)
 {
-    if (smem_image) return cmax <= 6 ? pick_L<MODE, true, 6>(L) : pick_L<MODE, true, 8>(L);
-    return cmax <= 6 ? pick_L<MODE, false, 6>(L) : pick_L<MODE, false, 8>(L);
+    if (img == 2) return cmax <= 6 ? pick_L<MODE, 2, 6>(L) : pick_L<MODE, 2, 8>(L);
+    if (img == 1) return cmax <= 6 ? pick_L<MODE, 1, 6>(L) : pick_L<MODE, 1, 8>(L);
+    return cmax <= 6 ? pick_L<MODE, 0, 6>(L) : pick_L<MODE, 0, 8>(L);
 }
 
 }  // namespace

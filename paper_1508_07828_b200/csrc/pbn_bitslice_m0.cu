@@ -3,6 +3,6 @@
 
 namespace pbn {
 
-const void* pick_bitslice_kernel_mode0(int L, bool smem_image, int cmax) { return pick_mode<0>(L, smem_image, cmax); }
+const void* pick_bitslice_kernel_mode0(int L, int img, int cmax) { return pick_mode<0>(L, img, cmax); }
 
 }  // namespace pbn

@@ -3,6 +3,6 @@
 
 namespace pbn {
 
-const void* pick_bitslice_kernel_mode1(int L, bool smem_image, int cmax) { return pick_mode<1>(L, smem_image, cmax); }
+const void* pick_bitslice_kernel_mode1(int L, int img, int cmax) { return pick_mode<1>(L, img, cmax); }
 
 }  // namespace pbn

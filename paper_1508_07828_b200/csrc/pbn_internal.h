@@ -247,6 +247,13 @@ struct BitsliceParams {
     int32_t any_off;           // from the group state base: any[2][32] words
     int32_t pq_off;            // from the group state base: [nquads + 1] uint4 per-quad Philox values (below)
     const uint32_t* geo_table; // geometric mode: Cg[0..n-1] (the main image's copy, global memory)
+    // cluster launch (IMG = 2): K CTAs per group, rank r's sub-image at
+    // T.image + c_img_off[r] (c_img_bytes[r] bytes, its erec / rounds at the
+    // given offsets), owning quads [c_qlo[r], c_qlo[r+1])
+    int32_t K;
+    uint32_t c_img_off[kMaxCluster], c_img_bytes[kMaxCluster], c_erec_off[kMaxCluster], c_rounds_off[kMaxCluster];
+    int32_t c_rounds[kMaxCluster];
+    int32_t c_qlo[kMaxCluster + 1];
 };
 // plane vectors per quad for the model's largest ell L
 inline int32_t bitslice_pv(int32_t L) { return (L >= 3 ? 2 : L == 2 ? 1 : 0) + 1; }
@@ -254,11 +261,16 @@ inline int32_t bitslice_pv(int32_t L) { return (L >= 3 ? 2 : L == 2 ? 1 : 0) + 1
 // 2 x 32 any words + 4 spare, 2 plane buffers of 4 PV words per quad, the
 // per-quad Philox table (4 words per quad: the part of rounds 1-2 that
 // depends only on the quad, the key and t_hi, computed once per work unit)
-inline int32_t bitslice_group_words(int32_t n_pad, int32_t L)
+// (nq_local: the quads of one CTA -- all of them, or a cluster CTA's share;
+// the any region: any[2][32], the cluster ranks' any words [2][16], a dummy)
+constexpr int32_t kBitsliceAnyWords = 100;
+inline int32_t bitslice_group_words(int32_t n_pad, int32_t L, int32_t nq_local = -1)
 {
-    return 3 * n_pad + 68 + 2 * bitslice_pv(L) * n_pad + n_pad + 4;
+    if (nq_local < 0) nq_local = n_pad / 4;
+    return 3 * n_pad + kBitsliceAnyWords + 2 * bitslice_pv(L) * 4 * nq_local + 4 * nq_local + 4;
 }
-const void* pick_bitslice_kernel(int mode, int L, bool smem_image, int cmax);
+// img: 0 image through L1/L2, 1 staged, 2 staged sub-image of a cluster (K1bc)
+const void* pick_bitslice_kernel(int mode, int L, int img, int cmax);
 // K1's default warps per group for ceil(n/4) quads (pbn_traj.cu)
 int default_group_warps(int nquads);
 

@@ -237,3 +237,72 @@ def test_geometric_launch_shapes_equal_K1(pbn, monkeypatch):
     assert pbn.pbn_last_kernel() == "K1b-global"
     for k in ALL:
         assert np.array_equal(g[k], ref[k]), ("global image", k)
+
+
+# K1bc: one 32-chain group per cluster of K CTAs (each owns a slice of the
+# quads and its sub-image; new words and any words exchanged through
+# distributed shared memory every step)
+@pytest.mark.parametrize("per_node", [False, True])
+@pytest.mark.parametrize("K", [2, 4, 8, 16])
+def test_cluster_equals_K1_and_oracle(pbn, K, per_node):
+    model, pred = config_model("C2"), config_predicate("C2")
+    pm = pbn.pbn_load(model, per_node=per_node)
+    kw = dict(n_chains=100, steps=500, burn_in=120, seed=12, batch=45)
+    ref = gpu_run(pm, model, pred, cluster_size=1, layout=1, schedule=1, **kw)
+    g = gpu_run(pm, model, pred, cluster_size=K, layout=BS, **kw)
+    assert pbn.pbn_last_kernel() == "K1bc"
+    for k in ALL:
+        assert np.array_equal(g[k], ref[k]), (K, k)
+    ids = sample_chain_ids(100, k=6, seed=K)
+    st, I, ws = oracle_run(model, pred, ids, steps=500, burn_in=120, seed=12, batch=45, per_node=per_node)
+    packed = pack_states(st)
+    for j, cid in enumerate(ids):
+        compare_chain(g, cid, packed[j], ws[j], 500, 45)
+
+
+@pytest.mark.parametrize("name,K", [("n5_ragged_quads", 2), ("n150_all_classes", 4), ("theta_8_classes", 2),
+                                    ("ell3_theta1_8", 8), ("heavy_perturbation", 4)])
+def test_cluster_models(pbn, name, K):
+    model, pred = {k: (m, p) for k, m, p in bs_models()}[name]
+    pm = pbn.pbn_load(model)
+    kw = dict(n_chains=45, steps=600, burn_in=77, seed=31, batch=40)
+    g = gpu_run(pm, model, pred, cluster_size=K, layout=BS, **kw)
+    assert pbn.pbn_last_kernel() == "K1bc"
+    st, I, ws = oracle_run(model, pred, np.arange(45), steps=600, burn_in=77, seed=31, batch=40)
+    packed = pack_states(st)
+    for c in range(45):
+        compare_chain(g, c, packed[c], ws[c], 600, 40)
+    assert np.array_equal(g["totals"], ostats.totals(ws))
+
+
+def test_cluster_geometric_and_multi_property(pbn):
+    model = config_model("C2")
+    rng = np.random.default_rng(5)
+    props = []
+    for _ in range(3):
+        k = int(rng.integers(1, 5))
+        props.append(Predicate(rng.choice(model.n, size=k, replace=False).astype(np.uint16),
+                               rng.integers(0, 2, size=k).astype(np.uint8)))
+    pm = pbn.pbn_load(model, geometric=True)
+    kw = dict(n_chains=70, steps=400, burn_in=50, seed=8, batch=25, props=props)
+    ref = gpu_run(pm, model, None, cluster_size=1, layout=1, **kw)
+    g = gpu_run(pm, model, None, cluster_size=4, layout=BS, **kw)
+    for k in ALL:
+        assert np.array_equal(g[k], ref[k]), k
+
+
+def test_cluster_C5_1024_sampled_chains(pbn):
+    """C5 at 1024 chains (its sweep point, 32 groups) through K1bc; the
+    oracle recomputes sampled chains at the full step count."""
+    c = CONFIGS["C5"]
+    model, pred = config_model("C5"), config_predicate("C5")
+    pm = pbn.pbn_load(model)
+    g = gpu_run(pm, model, pred, n_chains=1024, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch,
+                cluster_size=4, layout=BS)
+    assert pbn.pbn_last_kernel() == "K1bc"
+    ids = sample_chain_ids(1024, k=12, seed=c.sim_seed)
+    st, I, ws = oracle_run(model, pred, ids, steps=c.steps, burn_in=c.burn_in, seed=c.sim_seed, batch=c.batch,
+                           threads=os.cpu_count() or 8)
+    packed = pack_states(st)
+    for k, cid in enumerate(ids):
+        compare_chain(g, cid, packed[k], ws[k], c.steps, c.batch)
