@@ -148,20 +148,26 @@ typedef struct {
  *                touched word is overwritten
  *   bits_row_words  row stride of `bits` in u32 (0 = ceil(steps/32))
  *   groups_per_cta  0 or 1 (one 32-chain group per CTA in this build)
- *   warps_per_group warps sharing one group's nodes (0 = auto, <= 28 in this build)
+ *   warps_per_group warps sharing one group's nodes (0 = auto; <= 28 in this build,
+ *                <= 24 for the bit-sliced kernels)
  *   schedule     0 auto; 1 one CTA per group; 2 persistent CTAs pulling
  *                (group, chunk of chunk_steps steps) units, state carried
  *                between chunks in `workspace`
  *   chunk_steps  persistent chunk length (0 = auto)
  *   workspace    caller-owned device scratch (see pbn_simulate_workspace_size)
- *   layout       PBN_LAYOUT_*: chains over the lanes of a warp (K1 / K1c) or,
- *                for few chains, nodes over the threads of a cluster (K1n)
+ *   layout       PBN_LAYOUT_*: AUTO picks, per call: the bit-sliced kernel
+ *                (K1b, one group per CTA) when the groups fill the GPU and the
+ *                model has theta <= 8, ell <= 4, n <= 5460; for few groups its
+ *                cluster form (K1bc) or K1c; for <= 128 (256) chains K1n;
+ *                K1 otherwise.  CHAIN_LANES forces K1 / K1c, NODE_LANES K1n,
+ *                BITSLICE K1b (cluster_size >= 2: K1bc); pbn_last_kernel()
+ *                names the kernel a call ran
  *   chains_per_cluster  K1n: chains sharing one cluster (0 = auto)
- *   cluster_size 0: chosen per call -- one CTA per 32-chain group when the
- *                device image fits one CTA's shared memory and there are
- *                enough groups to fill the GPU, else a thread-block cluster of
- *                K CTAs per group (each stages 1/K of the image, the state is
- *                mirrored through distributed shared memory); 1 / K force it
+ *   cluster_size 0: chosen per call -- one CTA per 32-chain group when there
+ *                are enough groups to fill the GPU, else a thread-block
+ *                cluster of K CTAs per group (each stages 1/K of the image and
+ *                computes 1/K of the nodes, the state is mirrored through
+ *                distributed shared memory); 1 / K force it
  *   n_props, props  several properties from the same trajectories (the
  *                multi-property reuse of P:507-526): every statistic below is
  *                produced per property, property-major (property p's block
@@ -201,8 +207,9 @@ enum {
     PBN_LAYOUT_NODE_LANES = 2,  /* one chain per cluster of cluster_size CTAs (0 = auto), */
                                 /* threads over node quads, bit-packed state (K1n)     */
     PBN_LAYOUT_BITSLICE = 3     /* K1's group layout, functions evaluated bit-sliced    */
-                                /* over the 32 chains (K1b); models with theta <= 6,    */
-                                /* ell <= 4 and VECTOR / PER_NODE semantics only        */
+                                /* over the 32 chains (K1b; cluster_size >= 2: K1bc);   */
+                                /* models with theta <= 8, ell <= 4, n <= 5460; every   */
+                                /* semantics; PBN_E_USAGE outside that shape            */
 };
 
 /* Caller-owned DEVICE buffers, chain-major (row c = chain chain_base + c).
