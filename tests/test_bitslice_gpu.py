@@ -306,3 +306,33 @@ def test_cluster_C5_1024_sampled_chains(pbn):
     packed = pack_states(st)
     for k, cid in enumerate(ids):
         compare_chain(g, cid, packed[k], ws[k], c.steps, c.batch)
+
+
+@pytest.mark.parametrize("cluster", [1, 2])
+def test_edge_sizes(pbn, cluster):
+    """Zero recorded steps (burn-in only), one step, a batch longer than the
+    window, a ragged group: K1b (cluster 1) and K1bc (cluster 2)."""
+    model, pred = config_model("C2"), config_predicate("C2")
+    for n_chains, steps, burn_in, batch in [(33, 0, 50, 0), (40, 1, 0, 7), (70, 31, 1, 100), (5, 0, 0, 0)]:
+        full_compare(pbn, model, pred, n_chains=n_chains, steps=steps, burn_in=burn_in, seed=3, batch=batch,
+                     cluster_size=cluster)
+        assert pbn.pbn_last_kernel() == ("K1b" if cluster == 1 else "K1bc")
+
+
+def test_cluster_continuation_and_chain_split(pbn):
+    """K1bc continues chains exactly (init=False, step0 > 0, bits appended at
+    an offset) and splits chains across calls (chain_base)."""
+    model, pred = config_model("C3"), config_predicate("C3")
+    pm = pbn.pbn_load(model)
+    kw = dict(cluster_size=4, layout=BS)
+    full = gpu_run(pm, model, pred, n_chains=64, steps=480, seed=5, **kw)
+    s1 = gpu_run(pm, model, pred, n_chains=64, steps=200, seed=5, bits_row_words=15, **kw)
+    s2 = gpu_run(pm, model, pred, n_chains=64, steps=280, step0=200, seed=5, init=False, state=s1["state"],
+                 bits_offset=200, bits_row_words=15, bits_init=s1["bits"], **kw)
+    assert np.array_equal(s2["state"], full["state"])
+    assert np.array_equal(s2["bits"][:, :15], full["bits"][:, :15])
+    assert np.array_equal(s1["c1"].astype(np.int64) + s2["c1"], full["c1"])
+    a = gpu_run(pm, model, pred, n_chains=37, steps=480, seed=5, **kw)
+    b = gpu_run(pm, model, pred, n_chains=27, chain_base=37, steps=480, seed=5, **kw)
+    for k in ["state", "c1", "n01", "n10", "first_last", "bits"]:
+        assert np.array_equal(np.concatenate([a[k], b[k]]), full[k]), k
