@@ -412,7 +412,9 @@ std::vector<uint8_t> build_image(const pbn_model_desc* d, uint32_t Tp, pbn::Imag
                 const int32_t words = d->tbl_off[f + 1] - d->tbl_off[f];
                 const uint32_t off_t = B.alloc(4u * words, 4);
                 for (int32_t w = 0; w < words; ++w) B.u32(off_t)[w] = d->tables[d->tbl_off[f] + w];
-                const uint32_t off_p = B.alloc(4u * (size_t)std::max(theta, 1), 4);
+                // parent offsets 16-aligned and padded to whole 16-byte vectors
+                // (the generic path reads them four at a time)
+                const uint32_t off_p = B.alloc(16u * (size_t)((std::max(theta, 1) + 3) / 4), 16);
                 for (int32_t m = 0; m < theta; ++m) {
                     const uint32_t node = d->parents[d->par_off[f] + m];
                     B.u32(off_p)[m] = packed ? node : pbn::state_off(node, qs);

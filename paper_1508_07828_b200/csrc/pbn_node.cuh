@@ -281,11 +281,17 @@ __device__ PBN_SLOW_ATTR uint32_t slow_node_bit(const Img<SMEM>& img, uint32_t w
         if (j + step <= m1 && u > img.ld32(sr.x + 4u * (j + step - 1u))) j += step;
     const uint4 gd = img.ld128(sr.z + 16u * j);  // {toff, theta, poff, 0}
     uint32_t idx = 0;
-    for (uint32_t m = 0; m < sr.w; ++m) {
-        if (m < gd.y) {
-            const uint32_t off = img.ld32(gd.z + 4u * m);
-            const uint32_t wv = lds32(old + off);
-            idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+    // the parent offsets four at a time (poff 16-aligned, padded to whole
+    // vectors): one dependent image read per four parents, not per parent
+    for (uint32_t m = 0; m < sr.w; m += 4u) {
+        const uint4 o = img.ld128(gd.z + 4u * m);
+        const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4u; ++k) {
+            if (m + k < gd.y) {
+                const uint32_t wv = lds32(old + oo[k]);
+                idx = __funnelshift_l(__funnelshift_l(wv, wv, rot), idx, 1);
+            }
         }
     }
     const uint32_t tw = img.ld32(gd.x + 4u * (idx >> 5));
