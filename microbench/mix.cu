@@ -63,6 +63,37 @@ __global__ void __launch_bounds__(1024, 2) kmix(uint32_t seed)
                                  : "r"(s[k]));
             } else if (OP == 6) {  // LOP3 alone (reference)
                 asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[k]) : "r"(s[k]), "r"(lmask));
+            } else if (OP == 8) {  // 1 ISETP + 4 VOTE (the vote's own rate)
+                asm volatile(
+                    "{.reg .pred p; .reg .u32 a, b, c; setp.ne.u32 p, %0, 0; vote.sync.ballot.b32 a, p, 0xffffffff;"
+                    " vote.sync.ballot.b32 b, !p, 0xffffffff; vote.sync.ballot.b32 c, p, 0xffffffff;"
+                    " vote.sync.ballot.b32 %0, !p, 0xffffffff; add.u32 %1, a, b; add.u32 %1, %1, c;}"
+                    : "+r"(r[k]), "+r"(s[k]));
+            } else if (OP == 9) {  // ISETP + VOTE + 2 LOP3 (do the votes co-issue with the ALU pipe?)
+                asm volatile(
+                    "{.reg .pred p; setp.gt.u32 p, %0, %1; vote.sync.ballot.b32 %0, p, 0xffffffff;"
+                    " lop3.b32 %1, %1, %2, %1, 0x96; lop3.b32 %1, %1, %2, %0, 0x96;}"
+                    : "+r"(r[k]), "+r"(s[k])
+                    : "r"(lmask));
+            } else if (OP == 10) {  // ISETP + VOTE + 2 IMAD.WIDE + 2 LOP3 (phase A's mix)
+                asm volatile(
+                    "{.reg .pred p; .reg .u64 t; .reg .u32 h, l; setp.gt.u32 p, %0, %1; vote.sync.ballot.b32 h, p, 0xffffffff;"
+                    " mul.wide.u32 t, %0, 0xD2511F53; mov.b64 {l, %0}, t; lop3.b32 %0, %0, h, %2, 0x96;"
+                    " mul.wide.u32 t, %1, 0xCD9E8D57; mov.b64 {%1, h}, t; lop3.b32 %1, %1, h, l, 0x96;}"
+                    : "+r"(r[k]), "+r"(s[k])
+                    : "r"(lmask));
+            } else if (OP == 11) {  // phase A's ratio per node: 4 IMAD.WIDE, 5 LOP3, 3 ISETP, 2 VOTE (14 instr)
+                asm volatile(
+                    "{.reg .pred p, q; .reg .u64 t; .reg .u32 h, l, g;"
+                    " mul.wide.u32 t, %0, 0xD2511F53; mov.b64 {l, h}, t; lop3.b32 %0, h, %1, %2, 0x96;"
+                    " mul.wide.u32 t, %1, 0xCD9E8D57; mov.b64 {g, h}, t; lop3.b32 %1, h, l, %2, 0x96;"
+                    " mul.wide.u32 t, %0, 0xD2511F53; mov.b64 {l, h}, t; lop3.b32 %0, h, g, %2, 0x96;"
+                    " mul.wide.u32 t, %1, 0xCD9E8D57; mov.b64 {g, h}, t; lop3.b32 %1, h, l, %2, 0x96;"
+                    " setp.gt.u32 q, %0, g; setp.gt.xor.u32 p, %0, l, q; setp.gt.xor.u32 p, %0, h, p;"
+                    " vote.sync.ballot.b32 l, p, 0xffffffff; vote.sync.ballot.b32 h, q, 0xffffffff;"
+                    " lop3.b32 %1, %1, l, h, 0x96;}"
+                    : "+r"(r[k]), "+r"(s[k])
+                    : "r"(lmask));
             } else if (OP == 7) {  // LOP3 + IMAD (lo) 1:1 (reference: both pipes)
                 if (kk & 1)
                     asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[k]) : "r"(s[k]), "r"(lmask));
@@ -79,15 +110,19 @@ __global__ void __launch_bounds__(1024, 2) kmix(uint32_t seed)
 
 // SASS instructions per (kk) step of each OP, from cuobjdump of this file
 // (checked when run: the counts below are the ones the rate is divided by)
-static const double kInstPerStep[8] = {1.0, 2.0, 1.0, 3.0, 2.0, 1.5, 1.0, 1.0};
-static const char* kName[8] = {"IMAD.WIDE",
+static const double kInstPerStep[12] = {1.0, 2.0, 1.0, 3.0, 2.0, 1.5, 1.0, 1.0, 4.0625, 4.0, 6.0, 14.0};
+static const char* kName[12] = {"IMAD.WIDE",
                                "IMAD.WIDE + LOP3 (Philox round shape)",
                                "IMAD.HI",
                                "IMAD.HI + IMAD + LOP3",
                                "ISETP + VOTE",
                                "ISETP + VOTE + IMAD.WIDE (per 2 steps: 3 instr)",
                                "LOP3",
-                               "LOP3 + IMAD 1:1"};
+                               "LOP3 + IMAD 1:1",
+                               "ISETP + 4 VOTE + 2 IADD (7 instr)",
+                               "ISETP + VOTE + 2 LOP3 (4 instr)",
+                               "ISETP + VOTE + 2 IMAD.WIDE + 2 LOP3 (6 instr)",
+                               "phase-A ratio: 4 IMAD.WIDE + 5 LOP3 + 3 ISETP + 2 VOTE (14 instr)"};
 
 template <int OP>
 void run(int sms, double mhz)
@@ -121,5 +156,9 @@ int main(int argc, char** argv)
     run<5>(sms, mhz);
     run<6>(sms, mhz);
     run<7>(sms, mhz);
+    run<8>(sms, mhz);
+    run<9>(sms, mhz);
+    run<10>(sms, mhz);
+    run<11>(sms, mhz);
     return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
 }

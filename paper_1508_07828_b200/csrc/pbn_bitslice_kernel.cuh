@@ -56,13 +56,26 @@ namespace pbn {
 namespace {
 
 // 16-byte shared load ordered with the barriers (the per-quad Philox table
-// is refilled when t_hi changes)
+// is rewritten every step)
 __device__ __forceinline__ uint4 lds128_state(uint32_t a)
 {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+
+#if defined(PBN_BS_PRED_STORES)
+__device__ __forceinline__ void sts128_all(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w)
+{
+    sts128_if(a, x, y, z, w, (threadIdx.x & 31) == 0 ? FULL : 0u);
+}
+#else
+// 16-byte store of a warp-uniform vector by every lane (same address, same value)
+__device__ __forceinline__ void sts128_all(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+#endif
 
 // multiplexer tree: the sub-table of entries [B, B + 2^(C-K)) evaluated on
 // the parent words x[K..C-1] (x[0] = parents[0] = the index MSB, reading Q5):
@@ -370,19 +383,34 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                     if (L == 2) {
                         pb0[k] = __ballot_sync(FULL, u[k] > E1);
                     } else if (L == 3) {
-                        const bool p2 = u[k] > E2;
-                        pb0[k] = __ballot_sync(FULL, (u[k] > E1) != p2);
-                        pb1[k] = __ballot_sync(FULL, p2);
+                        // (the compare of E_2 shared by both planes: setp with
+                        // a predicate operand, 2 ISETP + 2 VOTE per node)
+                        asm volatile("{\n\t.reg .pred p2, p0;\n\t"
+                            "setp.gt.u32 p2, %2, %4;\n\t"
+                            "setp.gt.xor.u32 p0, %2, %3, p2;\n\t"
+                            "vote.sync.ballot.b32 %0, p0, 0xffffffff;\n\t"
+                            "vote.sync.ballot.b32 %1, p2, 0xffffffff;\n\t}"
+                            : "=r"(pb0[k]), "=r"(pb1[k])
+                            : "r"(u[k]), "r"(E1), "r"(E2));
                     } else if (L == 4) {
-                        const bool p2 = u[k] > E2;
-                        pb0[k] = __ballot_sync(FULL, ((u[k] > E1) != p2) != (u[k] > E3));
-                        pb1[k] = __ballot_sync(FULL, p2);
+                        // (3 ISETP + 2 VOTE per node; ptxas recomputes the E_2
+                        // compare when this is written with bools: 4 ISETP)
+                        asm volatile("{\n\t.reg .pred p2, p0;\n\t"
+                            "setp.gt.u32 p2, %2, %4;\n\t"
+                            "setp.gt.xor.u32 p0, %2, %3, p2;\n\t"
+                            "setp.gt.xor.u32 p0, %2, %5, p0;\n\t"
+                            "vote.sync.ballot.b32 %0, p0, 0xffffffff;\n\t"
+                            "vote.sync.ballot.b32 %1, p2, 0xffffffff;\n\t}"
+                            : "=r"(pb0[k]), "=r"(pb1[k])
+                            : "r"(u[k]), "r"(E1), "r"(E2), "r"(E3));
                     }
                 }
-                if (NP >= 1) sts128_if(pa, pb0[0], pb0[1], pb0[2], pb0[3], lead);
-                if (NP >= 2) sts128_if(pa + 16u, pb1[0], pb1[1], pb1[2], pb1[3], lead);
-                if (!GEO) sts128_if(pa + 16u * NP, 0u, 0u, 0u, 0u, lead);     // gamma (flagged quads: below)
-                sts128_if(gzb + QS * (uint32_t)q, 0u, 0u, 0u, 0u, lead);  // S_k's words, OR-ed in phase B
+                // (the ballots are warp-uniform: every lane stores the same
+                // vector to the same address, no predicate)
+                if (NP >= 1) sts128_all(pa, pb0[0], pb0[1], pb0[2], pb0[3]);
+                if (NP >= 2) sts128_all(pa + 16u, pb1[0], pb1[1], pb1[2], pb1[3]);
+                if (!GEO) sts128_all(pa + 16u * NP, 0u, 0u, 0u, 0u);     // gamma (flagged quads: below)
+                sts128_all(gzb + QS * (uint32_t)q, 0u, 0u, 0u, 0u);  // S_k's words, OR-ed in phase B
             };
             auto gammas = [&](const int q, const uint4 rq) {
                 const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
@@ -390,7 +418,19 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 any |= g0 | g1 | g2 | g3;
                 sts128_if(sel + 16u * (uint32_t)PV * (uint32_t)(q - qlo) + 16u * NP, g0, g1, g2, g3, lead);
             };
-            uint4 rw = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(q0 - qlo)), ps, P.rk);
+            // the per-(quad, step) Philox entries of this warp's quads (and of
+            // the quad after them, which the last iteration prefetches): one
+            // lane per quad; only this warp reads them (the neighbour warp
+            // writes the same value into the shared boundary entry)
+            // (uniform trip count and a predicated store: the warp stays
+            // provably converged for the ballots below)
+            for (int qb = q0; qb <= q1 && q0 < q1; qb += 32) {
+                const int qe = qb + lane;
+                const uint4 c = philox_quad_step_consts((uint32_t)qe, ps, P.rk);
+                sts128_if(pqt + 16u * (uint32_t)(qe - qlo), c.x, c.y, c.z, c.w, qe <= q1 ? FULL : 0u);
+            }
+            __syncwarp();
+            uint4 rw = philox_quad_ps(lds128_state(pqt + 16u * (uint32_t)(q0 - qlo)), ps, P.rk);
             uint4 e[3];
             for (int qc = q0; qc < qf; qc += 32) {
                 const int qe = min(qf, qc + 32);
@@ -401,12 +441,17 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 // and the Philox chain with the ballots
                 auto quad = [&](const int q, const uint4& cur, uint4& next) {
                     // (geometric stream: T_p = 0, no node word draws a perturbation)
-                    const uint32_t vq = GEO ? 0u : __ballot_sync(FULL, min(min(cur.x, cur.y), min(cur.z, cur.w)) < Tp);
+                    uint32_t vq = 0u;
+                    if (!GEO)
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+                            : "=r"(vq)
+                            : "r"(min(min(cur.x, cur.y), min(cur.z, cur.w))), "r"(Tp));
                     thresholds(q, e);
 #if defined(PBN_BS_SKIP_PHILOX)
                     next = make_uint4(cur.y * 3u + (uint32_t)q, cur.z ^ cur.x, cur.w + cur.y, cur.x * 5u);
 #else
-                    next = philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(q + 1 - qlo)), ps, P.rk);
+                    next = philox_quad_ps(lds128_state(pqt + 16u * (uint32_t)(q + 1 - qlo)), ps, P.rk);
 #endif
                     planes(q, cur, e);
                     if (!GEO)
@@ -429,7 +474,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                     const int jb = __ffs((int)gpend) - 1;
                     gpend &= gpend - 1;
                     const int qq = qe - 1 - jb;
-                    gammas(qq, philox_quad_pc(lds128_state(pqt + 16u * (uint32_t)(qq - qlo)), ps, P.rk));
+                    gammas(qq, philox_quad_ps(lds128_state(pqt + 16u * (uint32_t)(qq - qlo)), ps, P.rk));
                 }
             }
             if (qf < q1) {  // ragged last quad: padding nodes draw no perturbation
@@ -506,16 +551,6 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             }
         };
 
-        // the per-quad Philox table for t_hi of unit step k (all threads;
-        // the caller brackets it with barriers)
-        uint32_t table_thi = 0;
-        auto fill_table = [&](const int64_t k) {
-            table_thi = (uint32_t)((uint64_t)(P.step0 + r_begin - 1 + k) >> 32);
-            for (int q = tid; q <= qhi - qlo; q += blockDim.x) {  // local quads (+1: the prefetch of q + 1)
-                const uint4 c = philox_quad_consts((uint32_t)(qlo + q), table_thi, P.rk);
-                sts128_if(pqt + 16u * (uint32_t)q, c.x, c.y, c.z, c.w, FULL);
-            }
-        };
         // (PBN_BS_SKIP_A / PBN_BS_SKIP_B: timing-only builds that drop one
         // phase -- wrong outputs, used to split the step time between them)
 #if defined(PBN_BS_SKIP_A)
@@ -559,9 +594,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                                  "memory");
             }
         };
-        __syncthreads();  // the previous unit's phase A is done with the table
-        fill_table(1);
-        __syncthreads();
+        __syncthreads();  // the unit's S_0 is complete; the previous unit is done with the buffers
         if (K >= 1) phaseA(1, 16u);
         __syncthreads();
         exchange(0, 0u);  // (S_0 is complete in every CTA; this carries any(1))
@@ -569,12 +602,6 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         // of k+1; buffers ob = S_{k-1}, nb = S_k, zb = S_{k+1} rotate (uniform)
         uint32_t ob = 0u, nb = 16u, zb = 32u;
         for (int64_t k = 1; k <= K; ++k) {
-            // t_hi of step k + 1 changed (every 2^32 steps): refill the table
-            // first (uniform over the CTA; nobody reads it until phase A)
-            if (k < K && (uint32_t)((uint64_t)(P.step0 + r_begin + k) >> 32) != table_thi) {
-                fill_table(k + 1);
-                __syncthreads();
-            }
             if (k > 1) record(k - 1, ob);
             if (a_first) {
                 if (kA && k < K) phaseA(k + 1, zb);
