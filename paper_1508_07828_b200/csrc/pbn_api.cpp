@@ -523,9 +523,9 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
         const uint32_t to = B.alloc(stride * cnt, 16);
         for (size_t k = 0; k < cnt; ++k) {
             uint32_t* w = B.u32(to + stride * (uint32_t)k);
-            uint16_t* h = B.u16(to + stride * (uint32_t)k + 4u * T);  // [i << 2 | j, p_0 .. p_{c-1}]
+            uint16_t* h = B.u16(to + stride * (uint32_t)k + 4u * T);  // [state_off(i) | j, p_0 .. p_{c-1}]
             if (k >= cls[c].size()) {  // dummy task: table 0 contributes nothing
-                h[0] = (uint16_t)(((uint32_t)(4 * q_lo) << 2) | 1u);  // the first own node, function 1
+                h[0] = (uint16_t)(pbn::state_off((uint32_t)(4 * q_lo), pbn::kBitsliceQs) | 1u);  // the first own node, function 1
                 continue;
             }
             const int32_t i = cls[c][k].first, j = cls[c][k].second, f = d->fn_off[i] + j;
@@ -533,7 +533,7 @@ bool build_bitslice_image(const pbn_model_desc* d, uint32_t Tp, std::vector<uint
             // table padded to c index bits: padding parents are the low bits
             for (uint32_t e = 0; e < (1u << c); ++e)
                 w[e >> 5] |= table_bit(d, f, e >> (c - theta)) << (e & 31u);
-            h[0] = (uint16_t)(((uint32_t)i << 2) | (uint32_t)j);
+            h[0] = (uint16_t)(pbn::state_off((uint32_t)i, pbn::kBitsliceQs) | (uint32_t)j);
             for (int32_t m = 0; m < c; ++m)
                 h[1 + m] = (uint16_t)pbn::state_off(m < theta ? d->parents[d->par_off[f] + m] : 0u, pbn::kBitsliceQs);
         }

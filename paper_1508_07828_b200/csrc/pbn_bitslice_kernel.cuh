@@ -115,7 +115,7 @@ struct BImg {
 };
 
 // record stride of task class c (table words, then the u16 list
-// [i << 2 | j, p_0 .. p_{c-1}]; pbn_internal.h)
+// [state_off(i) | j, p_0 .. p_{c-1}]; pbn_internal.h)
 __host__ __device__ constexpr uint32_t bs_stride(int c) { return c <= 5 ? 16u : c <= 7 ? 32u : 64u; }
 
 // plane vectors per quad: NP selection-index planes (b0 = bit 0 of j, b1 =
@@ -126,12 +126,12 @@ struct Planes {
     static constexpr int PV = NP + 1;
 };
 
-// one round of 32 tasks of class C (theta = C parents), lane = task.  ob / nb
-// are the byte offsets of the old / new state buffer (uniform); the node's
+// one round of 32 tasks of class C (theta = C parents), lane = task.  gob / gnb
+// are the shared addresses of the old / new state buffer (uniform); the node's
 // plane words are at pl + 16 m (m < NP: b_m; m = NP: gamma).
 template <int C, int MODE, int L, bool SMEM>
-__device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uint32_t gob, uint32_t gnb, uint32_t sel,
-                                         uint32_t M, uint32_t qlo)
+__device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uint32_t gob, uint32_t gnb, uint32_t selq,
+                                         uint32_t M)
 {
     constexpr int T = C <= 5 ? 1 : (1 << C) / 32;      // table words
     constexpr int NV = (4 * T + 2 * (C + 1) + 15) / 16;  // 16-byte vectors of the record
@@ -148,7 +148,7 @@ __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uin
     uint32_t t[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) t[k] = k < T ? w[k] : 0u;
-    // u16 k of the list (0: i << 2 | j; 1 + m: parent m)
+    // u16 k of the list (0: state_off(i) | j; 1 + m: parent m)
     auto u16 = [&](int k) -> uint32_t {
         const uint32_t x = w[T + (k >> 1)];
         return (k & 1) ? x >> 16 : x & 0xFFFFu;
@@ -157,16 +157,23 @@ __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uin
 #pragma unroll
     for (int m = 0; m < C; ++m) x[m] = lds32_state(gob + u16(1 + m));
     const uint32_t F = mux_tree<0, C, 0>(t, x);
-    const uint32_t ij = u16(0);
-    const uint32_t i = ij >> 2, j = ij & 3u;
-    const uint32_t pl = sel + 16u * (uint32_t)PV * ((i >> 2) - qlo) + 4u * (i & 3u);  // (local quad)
+    // u16 0 = the node's state offset 48 (i >> 2) + 4 (i & 3) with j in its two
+    // low bits; with three plane vectors per quad it is also the offset of the
+    // node's plane words (selq = the plane buffer less the CTA's first quad)
+    const uint32_t h0 = u16(0);
+    const uint32_t so = h0 & 0xFFFCu, j = h0 & 3u;
+    uint32_t pl;
+    if constexpr (PV == 3)
+        pl = selq + so;
+    else
+        pl = selq + 16u * (uint32_t)PV * ((so * 43691u) >> 21) + (so & 12u);  // (so / 48: exact below 2^16)
     // selection plane of function j: the chains whose index bits equal j's
     const uint32_t b0 = NP >= 1 ? lds32_state(pl) : 0u;
     const uint32_t b1 = NP >= 2 ? lds32_state(pl + 16u) : 0u;
     const uint32_t gam = lds32_state(pl + 16u * NP);
     const uint32_t m0 = (j & 1u) - 1u, m1 = ((j >> 1) & 1u) - 1u;  // all ones where the bit of j is 0
     const uint32_t sj = (b0 ^ m0) & (NP >= 2 ? (b1 ^ m1) : m1);
-    const uint32_t out = state_off(i, kBitsliceQs);
+    const uint32_t out = so;
     const uint32_t old = lds32_state(gob + out);
     const uint32_t first = j == 0 ? FULL : 0u;  // function 0 carries the perturbation term
     uint32_t c;
@@ -409,8 +416,6 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 // vector to the same address, no predicate)
                 if (NP >= 1) sts128_all(pa, pb0[0], pb0[1], pb0[2], pb0[3]);
                 if (NP >= 2) sts128_all(pa + 16u, pb1[0], pb1[1], pb1[2], pb1[3]);
-                if (!GEO) sts128_all(pa + 16u * NP, 0u, 0u, 0u, 0u);     // gamma (flagged quads: below)
-                sts128_all(gzb + QS * (uint32_t)q, 0u, 0u, 0u, 0u);  // S_k's words, OR-ed in phase B
             };
             auto gammas = [&](const int q, const uint4 rq) {
                 const uint32_t g0 = __ballot_sync(FULL, rq.x < Tp), g1 = __ballot_sync(FULL, rq.y < Tp);
@@ -424,10 +429,16 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
             // writes the same value into the shared boundary entry)
             // (uniform trip count and a predicated store: the warp stays
             // provably converged for the ballots below)
+            // The same lanes zero their quad's gamma vector (flagged quads
+            // fill it below) and its words of S_k's buffer (OR-ed in phase B):
+            // one store per 32 quads instead of one per quad.
             for (int qb = q0; qb <= q1 && q0 < q1; qb += 32) {
                 const int qe = qb + lane;
                 const uint4 c = philox_quad_step_consts((uint32_t)qe, ps, P.rk);
                 sts128_if(pqt + 16u * (uint32_t)(qe - qlo), c.x, c.y, c.z, c.w, qe <= q1 ? FULL : 0u);
+                const uint32_t own = qe < q1 ? FULL : 0u;
+                if (!GEO) sts128_if(sel + 16u * (uint32_t)PV * (uint32_t)(qe - qlo) + 16u * NP, 0u, 0u, 0u, 0u, own);
+                sts128_if(gzb + QS * (uint32_t)qe, 0u, 0u, 0u, 0u, own);
             }
             __syncwarp();
             uint4 rw = philox_quad_ps(lds128_state(pqt + 16u * (uint32_t)(q0 - qlo)), ps, P.rk);
@@ -511,7 +522,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
 
         // ---- phase B of unit step k: S_k (buffer nb) from S_{k-1} (ob) and planes[k & 1] ----
         auto phaseB = [&](const int64_t k, const uint32_t ob, const uint32_t nb) {
-            const uint32_t sel = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes;
+            const uint32_t selq = sel0 + (uint32_t)(k & 1) * (uint32_t)B.sel_bytes - 16u * (uint32_t)PV * (uint32_t)qlo;
             const uint32_t gob = gbase + ob, gnb = gbase + nb;
             uint32_t M = 0;
             if (!PER_NODE) {
@@ -527,16 +538,16 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                 const uint2 rr = img.ld64(rounds + 8u * (uint32_t)rr_i);
                 const uint32_t ta = rr.x + (uint32_t)lane * bs_stride((int)rr.y);
                 switch (rr.y) {
-                    case 1: bs_round<1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
-                    case 2: bs_round<2, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
-                    case 3: bs_round<3, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
-                    case 4: bs_round<4, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
-                    case 5: bs_round<5, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
-                    case 6: bs_round<6, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 1: bs_round<1, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+                    case 2: bs_round<2, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+                    case 3: bs_round<3, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+                    case 4: bs_round<4, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+                    case 5: bs_round<5, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+                    case 6: bs_round<6, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
                     // classes 7 and 8 only in the CMAX = 8 kernels: their trees'
                     // registers would otherwise spill the theta <= 6 kernels
-                    case 7: if constexpr (CMAX >= 7) bs_round<CMAX >= 7 ? 7 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
-                    default: if constexpr (CMAX >= 8) bs_round<CMAX >= 8 ? 8 : 1, MODE, L, SMEM>(img, ta, gob, gnb, sel, M, (uint32_t)qlo); break;
+                    case 7: if constexpr (CMAX >= 7) bs_round<CMAX >= 7 ? 7 : 1, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+                    default: if constexpr (CMAX >= 8) bs_round<CMAX >= 8 ? 8 : 1, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
                 }
             }
         };

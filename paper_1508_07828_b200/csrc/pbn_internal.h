@@ -218,7 +218,7 @@ int max_active_nodepar_clusters(const NodeParParams& C, int threads, size_t smem
 //   tasks  per class c = max(theta, 1) = 1..8, padded to whole rounds of 32
 //          (dummy tasks: table 0, node 0, j 1), each record the 2^c-entry
 //          table in T = max(1, 2^c / 32) words (entry e at bit e & 31 of word
-//          e >> 5), then the u16 list [i << 2 | j, p_0 .. p_{c-1}]; stride 16
+//          e >> 5), then the u16 list [state_off(i, 48) | j, p_0 .. p_{c-1}]; stride 16
 //          bytes (c <= 5), 32 (c = 6, 7), 64 (c = 8).  idx = sum_m x(p_m)
 //          2^(c-1-m) (parents[0] the MSB, reading Q5); i = node, j = function
 //          index within the node, p_m = state_off(parent m, 48) (theta = 0
