@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     __shared__ __align__(8) uint64_t mbar;
 
     const int tid = threadIdx.x;
-    const int wg = tid >> 5;
+    const int wg = (int)__reduce_max_sync(FULL, (uint32_t)(tid >> 5));  // (warp-uniform for ptxas: no divergence guards on the votes)
     const int lane = tid & 31;
     const int W = P.warps_per_group;
     const int n = P.n;
@@ -264,8 +264,46 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     const uint32_t cany = anyw0 + 256u;  // cluster: any words of the ranks [2][16], then a dummy word
 
     const int NW = P.node_warps;
+#if defined(PBN_BS_NO_BALANCE)
     const int q0 = wg < NW ? qlo + (int)((int64_t)wg * (qhi - qlo) / NW) : qhi;
     const int q1 = wg < NW ? qlo + (int)((int64_t)(wg + 1) * (qhi - qlo) / NW) : qhi;
+#else
+    // Quads over the node warps so that every warp's step costs the same: the
+    // snake order gives the warps phase-B rounds of different classes (one
+    // class-6 round is worth ~4 quads of phase A), and all of them meet at
+    // one barrier per step.  Lane l works out warp l's share (instruction
+    // counts of the SASS bodies, per round / per quad); every warp computes
+    // the same split.  Outputs do not depend on it.
+    int q0, q1;
+    {
+        constexpr int kRoundCost[9] = {0, 50, 62, 78, 105, 160, 285, 540, 1050};
+        constexpr int kQuadCost = L >= 4 ? 74 : L == 3 ? 68 : L == 2 ? 58 : 48;
+        int cb = 0;
+        if (lane < W)
+            for (int m = 0; m * W < R; ++m) {
+                const int rr_i = (m & 1) ? (m + 1) * W - 1 - lane : m * W + lane;
+                if (rr_i < R) cb += kRoundCost[min(img.ld64(rounds + 8u * (uint32_t)rr_i).y, 8u)];
+            }
+        const int nq = qhi - qlo;
+        const int tot = (int)__reduce_add_sync(FULL, lane < NW ? (uint32_t)cb : 0u) + kQuadCost * nq;
+        // warp l's phase-A share x_l = T - cb_l (>= 0), T = tot / NW
+        int x = lane < NW ? max(tot / NW - cb, 0) : 0;
+        int sx = x;  // inclusive scan
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(FULL, sx, d);
+            if (lane >= d) sx += y;
+        }
+        const int st = __shfl_sync(FULL, sx, 31);
+        // cumulative rounding: warp l ends at round(nq S_l / S_tot), the last at nq
+        const int e1 = st > 0 ? (int)(((int64_t)sx * nq + st / 2) / st) : (int)((int64_t)(min(lane, NW - 1) + 1) * nq / NW);
+        const int e0 = __shfl_up_sync(FULL, e1, 1);
+        const int w_ = min(wg, 31);
+        const int a1 = __shfl_sync(FULL, e1, w_), a0 = wg == 0 ? 0 : __shfl_sync(FULL, e0, w_);
+        q0 = wg < NW ? qlo + a0 : qhi;
+        q1 = wg < NW ? qlo + a1 : qhi;
+    }
+#endif
     // all quads over the warps (the initial state: every CTA forms all of it)
     const int qi0 = (int)((int64_t)wg * P.nquads / W), qi1 = (int)((int64_t)(wg + 1) * P.nquads / W);
     const int nsw = P.state_words;
