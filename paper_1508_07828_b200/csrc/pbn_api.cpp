@@ -881,6 +881,8 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     plan.node_warps = std::min(W, P.nquads);
     plan.stats_warp0 = 0;
     plan.ctas = (int)((P.n_chains + 31) / 32);
+    Bp.rl_off = Bp.pq_off + 16 * (P.n_pad / 4 + 1);
+    Bp.rl_stride = (m->bs_rounds + W - 1) / W + 9;
     plan.threads = 32 * W;
     plan.smem_bytes = group_bytes + (smem_image ? m->bs_bytes : 0u);
     plan.image_in_smem = smem_image;
@@ -954,6 +956,12 @@ static pbn_status simulate_bitslice_cluster(pbn_model m, const pbn::TrajParams& 
     Bp.T.node_warps = std::min(W, std::max(use->max_lq, 1));
     Bp.T.stats_warp0 = 0;
     Bp.T.persistent = 0;
+    {
+        int32_t max_rounds = 0;
+        for (int r = 0; r < use->K; ++r) max_rounds = std::max(max_rounds, use->rounds[r]);
+        Bp.rl_off = Bp.pq_off + 16 * (use->max_lq + 1);
+        Bp.rl_stride = (max_rounds + W - 1) / W + 9;
+    }
     const size_t smem = smem_of(*use);
     const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, 2, m->bs_cmax);
     cudaError_t e = pbn::ensure_func_smem(fn, smem, use->K > 8);

@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     int q0, q1;
     {
         constexpr int kRoundCost[9] = {0, 50, 62, 78, 105, 160, 285, 540, 1050};
-        constexpr int kQuadCost = L >= 4 ? 74 : L == 3 ? 68 : L == 2 ? 58 : 48;
+#ifndef PBN_BS_QC
+#define PBN_BS_QC 74
+#endif
+        constexpr int kQuadCost = (L >= 4 ? 74 : L == 3 ? 68 : L == 2 ? 58 : 48) * PBN_BS_QC / 74;
         int cb = 0;
         if (lane < W)
             for (int m = 0; m * W < R; ++m) {
@@ -304,6 +307,27 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
         q1 = wg < NW ? qlo + a1 : qhi;
     }
 #endif
+    // This warp's phase-B rounds (the snake order over the round list, which
+    // is sorted by class, most expensive first) as a list of task offsets in
+    // shared memory, one sentinel after each class from CMAX down to 1: phase
+    // B walks it class by class with the class a compile-time constant (no
+    // per-round index arithmetic, round record, stride select or switch).
+    constexpr uint32_t kListEnd = 0xFFFFFFFFu;
+    const uint32_t rl = gbase + (uint32_t)B.rl_off + 4u * (uint32_t)(wg * B.rl_stride);
+    if (leader) {
+        uint32_t p = rl;
+        int c = CMAX;
+        for (int m = 0; m * W < R; ++m) {
+            const int rr_i = (m & 1) ? (m + 1) * W - 1 - wg : m * W + wg;
+            if (rr_i >= R) continue;
+            const uint2 rr = img.ld64(rounds + 8u * (uint32_t)rr_i);
+            for (; c > (int)rr.y; --c, p += 4u) sts32(p, kListEnd);
+            sts32(p, rr.x);
+            p += 4u;
+        }
+        for (; c >= 1; --c, p += 4u) sts32(p, kListEnd);
+    }
+    __syncwarp();
     // all quads over the warps (the initial state: every CTA forms all of it)
     const int qi0 = (int)((int64_t)wg * P.nquads / W), qi1 = (int)((int64_t)(wg + 1) * P.nquads / W);
     const int nsw = P.state_words;
@@ -570,24 +594,26 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
                     M = __reduce_or_sync(FULL, lane < W ? lds32(anyw0 + 128u * (uint32_t)(k & 1) + 4u * lane) : 0u) &
                         vmask;
             }
-            for (int m = 0; m * W < R; ++m) {
-                const int rr_i = (m & 1) ? (m + 1) * W - 1 - wg : m * W + wg;
-                if (rr_i >= R) continue;
-                const uint2 rr = img.ld64(rounds + 8u * (uint32_t)rr_i);
-                const uint32_t ta = rr.x + (uint32_t)lane * bs_stride((int)rr.y);
-                switch (rr.y) {
-                    case 1: bs_round<1, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    case 2: bs_round<2, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    case 3: bs_round<3, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    case 4: bs_round<4, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    case 5: bs_round<5, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    case 6: bs_round<6, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    // classes 7 and 8 only in the CMAX = 8 kernels: their trees'
-                    // registers would otherwise spill the theta <= 6 kernels
-                    case 7: if constexpr (CMAX >= 7) bs_round<CMAX >= 7 ? 7 : 1, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
-                    default: if constexpr (CMAX >= 8) bs_round<CMAX >= 8 ? 8 : 1, MODE, L, SMEM>(img, ta, gob, gnb, selq, M); break;
+            uint32_t p = rl;
+            auto run_class = [&](auto cc) {
+                constexpr int C = decltype(cc)::value;
+                for (;;) {
+                    const uint32_t tb = lds32(p);
+                    p += 4u;
+                    if (tb == kListEnd) break;
+                    bs_round<C, MODE, L, SMEM>(img, tb + (uint32_t)lane * bs_stride(C), gob, gnb, selq, M);
                 }
-            }
+            };
+            // classes 7 and 8 only in the CMAX = 8 kernels: their trees'
+            // registers would otherwise spill the theta <= 6 kernels
+            if constexpr (CMAX >= 8) run_class(std::integral_constant<int, 8>{});
+            if constexpr (CMAX >= 7) run_class(std::integral_constant<int, 7>{});
+            run_class(std::integral_constant<int, 6>{});
+            run_class(std::integral_constant<int, 5>{});
+            run_class(std::integral_constant<int, 4>{});
+            run_class(std::integral_constant<int, 3>{});
+            run_class(std::integral_constant<int, 2>{});
+            run_class(std::integral_constant<int, 1>{});
         };
 
         // statistics of unit step k (S_k in the buffer at byte offset buf), statistics warps

@@ -246,6 +246,8 @@ struct BitsliceParams {
     int32_t sel_bytes;         // bytes of one plane buffer (16 PV nquads)
     int32_t any_off;           // from the group state base: any[2][32] words
     int32_t pq_off;            // from the group state base: [nquads + 1] uint4 per-quad Philox values (below)
+    int32_t rl_off;            // from the group state base: the warps' phase-B round lists (below)
+    int32_t rl_stride;         // words per warp: ceil(rounds / warps) + 9
     const uint32_t* geo_table; // geometric mode: Cg[0..n-1] (the main image's copy, global memory)
     // cluster launch (IMG = 2): K CTAs per group, rank r's sub-image at
     // T.image + c_img_off[r] (c_img_bytes[r] bytes, its erec / rounds at the
@@ -264,10 +266,20 @@ inline int32_t bitslice_pv(int32_t L) { return (L >= 3 ? 2 : L == 2 ? 1 : 0) + 1
 // (nq_local: the quads of one CTA -- all of them, or a cluster CTA's share;
 // the any region: any[2][32], the cluster ranks' any words [2][16], a dummy)
 constexpr int32_t kBitsliceAnyWords = 100;
+// the warps' phase-B round lists: per warp its rounds' task offsets in class
+// order, one sentinel after each class (built once per CTA): at most
+// rounds + 10 warps words, rounds <= 16 nq / 32 + 8 (four functions per node,
+// one partial round per class)
+// (a multiple of 4 words: the staged image after the group state is 16-byte aligned)
+inline int32_t bitslice_round_list_words(int32_t nq_local)
+{
+    return (nq_local / 2 + 8 + 10 * (PBN_BS_THREADS / 32) + 3) & ~3;
+}
 inline int32_t bitslice_group_words(int32_t n_pad, int32_t L, int32_t nq_local = -1)
 {
     if (nq_local < 0) nq_local = n_pad / 4;
-    return 3 * n_pad + kBitsliceAnyWords + 2 * bitslice_pv(L) * 4 * nq_local + 4 * nq_local + 4;
+    return 3 * n_pad + kBitsliceAnyWords + 2 * bitslice_pv(L) * 4 * nq_local + 4 * nq_local + 4 +
+           bitslice_round_list_words(nq_local);
 }
 // img: 0 image through L1/L2, 1 staged, 2 staged sub-image of a cluster (K1bc)
 const void* pick_bitslice_kernel(int mode, int L, int img, int cmax);
