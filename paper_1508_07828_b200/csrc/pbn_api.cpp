@@ -872,8 +872,10 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     Bp.sel_off = 12 * P.n_pad + 4 * pbn::kBitsliceAnyWords;
     Bp.sel_bytes = 4 * pbn::bitslice_pv(m->bs_L) * P.n_pad;
     Bp.pq_off = Bp.sel_off + 2 * Bp.sel_bytes;
-    // all the budget's warps (24: profiles/ in DESIGN §11)
-    int W = a->warps_per_group > 0 ? a->warps_per_group : std::min(pbn::kBitsliceMaxWarps, std::max(P.nquads, 1));
+    // 20 warps on the staged image, all 24 of the budget on the global image
+    int W = a->warps_per_group > 0
+                ? a->warps_per_group
+                : std::min(smem_image ? pbn::kBitsliceSmallWarps : pbn::kBitsliceMaxWarps, std::max(P.nquads, 1));
     W = std::max(W, P.n_props);
     if (W > pbn::kBitsliceMaxWarps || W > std::max(P.nquads, P.n_props)) return PBN_E_USAGE;
     pbn::LaunchPlan plan;
@@ -892,7 +894,7 @@ static pbn_status simulate_bitslice(pbn_model m, const pbn::TrajParams& P, const
     if (a->schedule < 0 || a->schedule > 2 || a->chunk_steps < 0 || a->workspace_bytes < 0) return PBN_E_USAGE;
     if (P.geometric) Bp.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->geo_off);
     const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, smem_image ? 1 : 0,
-                                               m->bs_cmax);
+                                               m->bs_cmax, plan.threads);
     const int rc = pbn::launch_group_units(Bp.T, fn, &Bp, plan, m->device, a->schedule, a->chunk_steps, a->workspace,
                                            (size_t)a->workspace_bytes, stream);
     if (rc == -2) return PBN_E_USAGE;
@@ -949,7 +951,7 @@ static pbn_status simulate_bitslice_cluster(pbn_model m, const pbn::TrajParams& 
     for (int r = 0; r <= use->K; ++r) Bp.c_qlo[r] = use->qlo[r];
     if (P.geometric) Bp.geo_table = reinterpret_cast<const uint32_t*>(m->d_image + m->geo_off);
     int W = a->warps_per_group > 0 ? a->warps_per_group
-                                   : std::min(pbn::kBitsliceMaxWarps, std::max(use->max_lq, 1));
+                                   : std::min(pbn::kBitsliceSmallWarps, std::max(use->max_lq, 1));
     W = std::max(W, P.n_props);
     if (W > pbn::kBitsliceMaxWarps) return PBN_E_USAGE;
     Bp.T.warps_per_group = W;
@@ -963,7 +965,7 @@ static pbn_status simulate_bitslice_cluster(pbn_model m, const pbn::TrajParams& 
         Bp.rl_stride = (max_rounds + W - 1) / W + 9;
     }
     const size_t smem = smem_of(*use);
-    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, 2, m->bs_cmax);
+    const void* fn = pbn::pick_bitslice_kernel(P.per_node ? 1 : P.geometric ? 2 : 0, m->bs_L, 2, m->bs_cmax, 32 * W);
     cudaError_t e = pbn::ensure_func_smem(fn, smem, use->K > 8);
     if (e != cudaSuccess) return PBN_E_CUDA;
     cudaLaunchConfig_t cfg = {};

@@ -4,15 +4,15 @@
 
 namespace pbn {
 
-const void* pick_bitslice_kernel_mode0(int L, int img, int cmax);
-const void* pick_bitslice_kernel_mode1(int L, int img, int cmax);
-const void* pick_bitslice_kernel_mode2(int L, int img, int cmax);
+const void* pick_bitslice_kernel_mode0(int L, int img, int cmax, int threads);
+const void* pick_bitslice_kernel_mode1(int L, int img, int cmax, int threads);
+const void* pick_bitslice_kernel_mode2(int L, int img, int cmax, int threads);
 
-const void* pick_bitslice_kernel(int mode, int L, int img, int cmax)
+const void* pick_bitslice_kernel(int mode, int L, int img, int cmax, int threads)
 {
-    return mode == 1   ? pick_bitslice_kernel_mode1(L, img, cmax)
-           : mode == 2 ? pick_bitslice_kernel_mode2(L, img, cmax)
-                       : pick_bitslice_kernel_mode0(L, img, cmax);
+    return mode == 1   ? pick_bitslice_kernel_mode1(L, img, cmax, threads)
+           : mode == 2 ? pick_bitslice_kernel_mode2(L, img, cmax, threads)
+                       : pick_bitslice_kernel_mode0(L, img, cmax, threads);
 }
 
 }  // namespace pbn

@@ -182,9 +182,8 @@ __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uin
     } else {          // VECTOR: chains with any gamma take s XOR gamma
         c = (F & sj & ~M) | ((old ^ gam) & M & first);
     }
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(gnb + out),
-                 "r"(c)
-                 : "memory");
+    // (unconditional: a zero word is rare, and the predicated form costs a branch)
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(gnb + out), "r"(c) : "memory");
 }
 
 // MODE: 0 VECTOR, 1 PER_NODE, 2 geometric; L = the model's largest ell;
@@ -194,8 +193,11 @@ __device__ __forceinline__ void bs_round(const BImg<SMEM>& img, uint32_t ta, uin
 // step's barrier, pushes its nodes' new words (and its any word) into every
 // peer through distributed shared memory before one cluster barrier;
 // CMAX: the largest task class (6 or 8)
-template <int MODE, int L, int IMG, int CMAX>
-__global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
+// TB: the thread budget (768 = 24 warps x 80 registers, or 640 = 20 warps x
+// ~94 registers: the staged-image kernels run faster with the latter, the
+// global-image kernel needs the warps to cover its L1/L2 reads)
+template <int MODE, int L, int IMG, int CMAX, int TB>
+__global__ void __launch_bounds__(TB, 1) bitslice_kernel(const __grid_constant__ BitsliceParams B)
 {
     constexpr bool SMEM = IMG != 0;
     constexpr bool CLU = IMG == 2;
@@ -276,11 +278,8 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     // the same split.  Outputs do not depend on it.
     int q0, q1;
     {
-        constexpr int kRoundCost[9] = {0, 50, 62, 78, 105, 160, 285, 540, 1050};
-#ifndef PBN_BS_QC
-#define PBN_BS_QC 74
-#endif
-        constexpr int kQuadCost = (L >= 4 ? 74 : L == 3 ? 68 : L == 2 ? 58 : 48) * PBN_BS_QC / 74;
+        constexpr int kRoundCost[9] = {0, 37, 48, 62, 90, 145, 270, 525, 1035};
+        constexpr int kQuadCost = L >= 4 ? 68 : L == 3 ? 62 : L == 2 ? 52 : 42;
         int cb = 0;
         if (lane < W)
             for (int m = 0; m * W < R; ++m) {
@@ -730,24 +729,29 @@ __global__ void __launch_bounds__(PBN_BS_THREADS, 1) bitslice_kernel(const __gri
     }
 }
 
-template <int MODE, int IMG, int CMAX>
+template <int MODE, int IMG, int CMAX, int TB>
 const void* pick_L(int L)
 {
     switch (L) {
-        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1, IMG, CMAX>);
-        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2, IMG, CMAX>);
-        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3, IMG, CMAX>);
-        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4, IMG, CMAX>);
+        case 1: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 1, IMG, CMAX, TB>);
+        case 2: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 2, IMG, CMAX, TB>);
+        case 3: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 3, IMG, CMAX, TB>);
+        default: return reinterpret_cast<const void*>(&bitslice_kernel<MODE, 4, IMG, CMAX, TB>);
     }
 }
 
-// img: 0 global image, 1 staged, 2 staged sub-image of a cluster
+// img: 0 global image, 1 staged, 2 staged sub-image of a cluster; threads: the
+// launch's block size (the staged kernels have a 640-thread build)
 template <int MODE>
-const void* pick_mode(int L, int img, int cmax)
+const void* pick_mode(int L, int img, int cmax, int threads)
 {
-    if (img == 2) return cmax <= 6 ? pick_L<MODE, 2, 6>(L) : pick_L<MODE, 2, 8>(L);
-    if (img == 1) return cmax <= 6 ? pick_L<MODE, 1, 6>(L) : pick_L<MODE, 1, 8>(L);
-    return cmax <= 6 ? pick_L<MODE, 0, 6>(L) : pick_L<MODE, 0, 8>(L);
+    if (img != 0 && threads <= kBitsliceSmallThreads) {
+        if (img == 2) return cmax <= 6 ? pick_L<MODE, 2, 6, kBitsliceSmallThreads>(L) : pick_L<MODE, 2, 8, kBitsliceSmallThreads>(L);
+        return cmax <= 6 ? pick_L<MODE, 1, 6, kBitsliceSmallThreads>(L) : pick_L<MODE, 1, 8, kBitsliceSmallThreads>(L);
+    }
+    if (img == 2) return cmax <= 6 ? pick_L<MODE, 2, 6, PBN_BS_THREADS>(L) : pick_L<MODE, 2, 8, PBN_BS_THREADS>(L);
+    if (img == 1) return cmax <= 6 ? pick_L<MODE, 1, 6, PBN_BS_THREADS>(L) : pick_L<MODE, 1, 8, PBN_BS_THREADS>(L);
+    return cmax <= 6 ? pick_L<MODE, 0, 6, PBN_BS_THREADS>(L) : pick_L<MODE, 0, 8, PBN_BS_THREADS>(L);
 }
 
 }  // namespace

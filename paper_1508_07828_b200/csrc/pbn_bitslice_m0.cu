@@ -3,6 +3,9 @@
 
 namespace pbn {
 
-const void* pick_bitslice_kernel_mode0(int L, int img, int cmax) { return pick_mode<0>(L, img, cmax); }
+const void* pick_bitslice_kernel_mode0(int L, int img, int cmax, int threads)
+{
+    return pick_mode<0>(L, img, cmax, threads);
+}
 
 }  // namespace pbn

@@ -237,6 +237,13 @@ constexpr uint32_t kBitsliceQs = 48;     // bytes between quads: three interleav
 #define PBN_BS_THREADS 768
 #endif
 constexpr int kBitsliceMaxWarps = PBN_BS_THREADS / 32;
+// the staged-image kernels' second build: 640 threads = 20 warps at ~94
+// registers (C4 7.97e11 -> 8.08e11, C3 7.03e11 -> 7.28e11 node-updates/s; warp
+// counts that are not a multiple of the 4 schedulers lose 8 %); the default
+// when the image is staged.  The global-image kernel keeps 24 warps (C5
+// 5.87e11 vs 5.77e11 at 20)
+constexpr int kBitsliceSmallThreads = 640;
+constexpr int kBitsliceSmallWarps = kBitsliceSmallThreads / 32;
 struct BitsliceParams {
     TrajParams T;              // T.image = the bitslice image
     uint32_t erec_off;         // image offsets
@@ -282,7 +289,8 @@ inline int32_t bitslice_group_words(int32_t n_pad, int32_t L, int32_t nq_local =
            bitslice_round_list_words(nq_local);
 }
 // img: 0 image through L1/L2, 1 staged, 2 staged sub-image of a cluster (K1bc)
-const void* pick_bitslice_kernel(int mode, int L, int img, int cmax);
+// threads: the launch's block size (staged images: a 640-thread build for <= 20 warps)
+const void* pick_bitslice_kernel(int mode, int L, int img, int cmax, int threads);
 // K1's default warps per group for ceil(n/4) quads (pbn_traj.cu)
 int default_group_warps(int nquads);
 
