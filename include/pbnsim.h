@@ -149,7 +149,8 @@ typedef struct {
  *   bits_row_words  row stride of `bits` in u32 (0 = ceil(steps/32))
  *   groups_per_cta  0 or 1 (one 32-chain group per CTA in this build)
  *   warps_per_group warps sharing one group's nodes (0 = auto; <= 28 in this build,
- *                <= 24 for the bit-sliced kernels)
+ *                <= 24 for the bit-sliced kernels, whose auto is 20 on a
+ *                staged image and 24 on a global one)
  *   schedule     0 auto; 1 one CTA per group; 2 persistent CTAs pulling
  *                (group, chunk of chunk_steps steps) units, state carried
  *                between chunks in `workspace`

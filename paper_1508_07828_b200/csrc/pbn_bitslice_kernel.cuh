@@ -11,13 +11,17 @@
 // chains instead of once per chain:
 //
 //   phase A (lane = chain; every warp its quads of nodes, as K1):
-//     one Philox4x32-10 call per quad (A3, reading Q2); per node the
-//     selection planes s_m = ballot(u > E_m), m = 1..L-1 (A5: chain l picks
-//     function j = #{m : u_l > E_m}, so bit l of s_j & ~s_{j+1} is set iff
-//     chain l picks j); one vote per quad flags the ~1 % of quads where some
-//     chain drew u < T_p, whose gamma words (A4) are formed after the quad
-//     loop; per quad the planes and gamma words go to L 16-byte vectors, and
-//     the warp zeroes its quads' words of the step's state buffer.
+//     one Philox4x32-10 call per quad (A3, reading Q2), finished from a per-
+//     (quad, step) table entry that one lane per quad computes once per step
+//     (rounds 1-2 and the lane-uniform M0 product of round 3; pbn_node.cuh:
+//     philox_quad_step_consts / philox_quad_ps); per node the bits of the
+//     selected index j = #{m : u > E_m} as ballots (A5: b_0 = the parity of
+//     the compares, b_1 = [u > E_2]; phase B takes the chains whose index
+//     bits equal a function's j); one vote per quad flags the ~1 % of quads
+//     where some chain drew u < T_p, whose gamma words (A4) are formed after
+//     the quad loop; per quad the plane vectors are stored by every lane
+//     (warp-uniform values, no predicate), the gamma and next-state zero
+//     vectors for 32 quads at once before the loop.
 //   phase B (lane = task = one predictor function of one node):
 //     the parents' bit-sliced words are gathered (A6: one LDS per parent for
 //     all 32 chains), the function's truth table is evaluated on them as a
@@ -36,6 +40,10 @@
 // any words are double-buffered by step parity and the state triple-buffered
 // (B(t) reads S_{t-1}, ORs into S_t; A(t+1) zeroes S_{t+1}'s buffer; the
 // statistics warp reads S_t in the next interval).
+//
+// The quads are split over the warps by each warp's phase-B round cost (all
+// warps meet at the one barrier per step), and phase B walks a per-warp list
+// of its rounds class by class (the class a compile-time constant).
 //
 // Per node-update the work is one quarter of a Philox call, L-1 compare +
 // ballot pairs and ~1/32 of the task's gather and tree instead
@@ -511,6 +519,44 @@ __global__ void __launch_bounds__(TB, 1) bitslice_kernel(const __grid_constant__
                 // next quad's Philox call and the plane ballots follow it in
                 // one basic block, so the scheduler overlaps the loads' latency
                 // and the Philox chain with the ballots
+#if defined(PBN_BS_PAIRFLAG)
+                // (variant: the flag vote once per PAIR of quads: part 0 leaves
+                // the minimum of its words in mq, part 1 votes on the minimum of
+                // all eight and flags both quads; part 2 = a single quad)
+                uint32_t mq = 0u;
+                auto quad = [&](const int q, const uint4& cur, uint4& next, const int part) {
+                    uint32_t vq = 0u;
+                    if (!GEO) {
+                        const uint32_t m4 = min(min(cur.x, cur.y), min(cur.z, cur.w));
+                        if (part == 0)
+                            mq = m4;
+                        else
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+                                : "=r"(vq)
+                                : "r"(part == 1 ? min(mq, m4) : m4), "r"(Tp));
+                    }
+                    thresholds(q, e);
+                    next = philox_quad_ps(lds128_state(pqt + 16u * (uint32_t)(q + 1 - qlo)), ps, P.rk);
+                    planes(q, cur, e);
+                    if (!GEO) {
+                        if (part == 1)
+                            asm("{\n\t.reg .u32 f;\n\tmin.u32 f, %1, 1;\n\tmul.lo.u32 f, f, 3;\n\tmad.lo.u32 %0, %0, 4, f;\n\t}" : "+r"(gpend) : "r"(vq));
+                        else if (part == 2)
+                            asm("{\n\t.reg .u32 f;\n\tmin.u32 f, %1, 1;\n\tmad.lo.u32 %0, %0, 2, f;\n\t}" : "+r"(gpend) : "r"(vq));
+                    }
+                };
+                int q = qc;
+                uint4 rn;
+                for (; q + 1 < qe; q += 2) {
+                    quad(q, rw, rn, 0);
+                    quad(q + 1, rn, rw, 1);
+                }
+                if (q < qe) {
+                    quad(q, rw, rn, 2);
+                    rw = rn;
+                }
+#else
                 auto quad = [&](const int q, const uint4& cur, uint4& next) {
                     // (geometric stream: T_p = 0, no node word draws a perturbation)
                     uint32_t vq = 0u;
@@ -541,6 +587,7 @@ __global__ void __launch_bounds__(TB, 1) bitslice_kernel(const __grid_constant__
                     quad(q, rw, rn);
                     rw = rn;
                 }
+#endif
                 // flagged quads: their gamma words (A4)
                 while (gpend) {
                     const int jb = __ffs((int)gpend) - 1;

@@ -268,8 +268,9 @@ struct BitsliceParams {
 inline int32_t bitslice_pv(int32_t L) { return (L >= 3 ? 2 : L == 2 ? 1 : 0) + 1; }
 // group shared memory of the bitslice kernel (u32 words): 3 state buffers,
 // 2 x 32 any words + 4 spare, 2 plane buffers of 4 PV words per quad, the
-// per-quad Philox table (4 words per quad: the part of rounds 1-2 that
-// depends only on the quad, the key and t_hi, computed once per work unit)
+// per-quad Philox table (4 words per quad: the lane-uniform part of rounds
+// 1-3 for the current step, rewritten by the quad's warp every step), the
+// warps' phase-B round lists
 // (nq_local: the quads of one CTA -- all of them, or a cluster CTA's share;
 // the any region: any[2][32], the cluster ranks' any words [2][16], a dummy)
 constexpr int32_t kBitsliceAnyWords = 100;

@@ -1,5 +1,5 @@
 # evidence pass (round 2, K1b): tests, smoke, every bench line, launch list, DRAM traffic, one ncu --set full of K1b
-TAG=${1:-r3q}
+TAG=${1:-r6z}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 timeout 2400 python -m pytest tests -m gpu -q -rf --durations=10 > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/pytest_gpu_$TAG.log
