@@ -35,8 +35,8 @@
 //   statistics (A8-A10): as K1, on the committed words.
 //
 // Phase A reads no state, so phase A of step t+1 shares an interval with
-// phase B of step t (even warps A first, odd warps B first, so the pipes see
-// both instruction mixes at once): one CTA barrier per step; the planes and
+// phase B of step t (half of each scheduler's warps A first, the others B
+// first, so the pipes see both instruction mixes at once): one CTA barrier per step; the planes and
 // any words are double-buffered by step parity and the state triple-buffered
 // (B(t) reads S_{t-1}, ORs into S_t; A(t+1) zeroes S_{t+1}'s buffer; the
 // statistics warp reads S_t in the next interval).
@@ -342,7 +342,12 @@ __global__ void __launch_bounds__(TB, 1) bitslice_kernel(const __grid_constant__
     const int64_t total = P.burn_in + P.steps;
     const uint32_t Tp = P.Tp;
     const bool full_quads = (n & 3) == 0 || q1 < P.nquads;
-    const bool a_first = (wg & 1) == 0;  // even warps: A(t+1) then B(t); odd: B(t) then A(t+1)
+    // half of the warps run A(t+1) then B(t), the others B(t) then A(t+1),
+    // alternating among the warps of one scheduler (warp w issues on scheduler
+    // w % 4), so every scheduler sees both instruction mixes at once (by warp
+    // parity instead -- the same order on all of a scheduler's warps -- C5
+    // loses 2-3 %, C4 / C3 0.4 %; all warps A first: C4 -1 %)
+    const bool a_first = ((wg >> 2) & 1) == 0;
     __shared__ unsigned long long s_unit;
 
     for (int64_t it = 0;; ++it) {
@@ -519,44 +524,6 @@ __global__ void __launch_bounds__(TB, 1) bitslice_kernel(const __grid_constant__
                 // next quad's Philox call and the plane ballots follow it in
                 // one basic block, so the scheduler overlaps the loads' latency
                 // and the Philox chain with the ballots
-#if defined(PBN_BS_PAIRFLAG)
-                // (variant: the flag vote once per PAIR of quads: part 0 leaves
-                // the minimum of its words in mq, part 1 votes on the minimum of
-                // all eight and flags both quads; part 2 = a single quad)
-                uint32_t mq = 0u;
-                auto quad = [&](const int q, const uint4& cur, uint4& next, const int part) {
-                    uint32_t vq = 0u;
-                    if (!GEO) {
-                        const uint32_t m4 = min(min(cur.x, cur.y), min(cur.z, cur.w));
-                        if (part == 0)
-                            mq = m4;
-                        else
-                            asm volatile(
-                                "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
-                                : "=r"(vq)
-                                : "r"(part == 1 ? min(mq, m4) : m4), "r"(Tp));
-                    }
-                    thresholds(q, e);
-                    next = philox_quad_ps(lds128_state(pqt + 16u * (uint32_t)(q + 1 - qlo)), ps, P.rk);
-                    planes(q, cur, e);
-                    if (!GEO) {
-                        if (part == 1)
-                            asm("{\n\t.reg .u32 f;\n\tmin.u32 f, %1, 1;\n\tmul.lo.u32 f, f, 3;\n\tmad.lo.u32 %0, %0, 4, f;\n\t}" : "+r"(gpend) : "r"(vq));
-                        else if (part == 2)
-                            asm("{\n\t.reg .u32 f;\n\tmin.u32 f, %1, 1;\n\tmad.lo.u32 %0, %0, 2, f;\n\t}" : "+r"(gpend) : "r"(vq));
-                    }
-                };
-                int q = qc;
-                uint4 rn;
-                for (; q + 1 < qe; q += 2) {
-                    quad(q, rw, rn, 0);
-                    quad(q + 1, rn, rw, 1);
-                }
-                if (q < qe) {
-                    quad(q, rw, rn, 2);
-                    rw = rn;
-                }
-#else
                 auto quad = [&](const int q, const uint4& cur, uint4& next) {
                     // (geometric stream: T_p = 0, no node word draws a perturbation)
                     uint32_t vq = 0u;
@@ -587,7 +554,6 @@ __global__ void __launch_bounds__(TB, 1) bitslice_kernel(const __grid_constant__
                     quad(q, rw, rn);
                     rw = rn;
                 }
-#endif
                 // flagged quads: their gamma words (A4)
                 while (gpend) {
                     const int jb = __ffs((int)gpend) - 1;
