@@ -94,40 +94,6 @@ __device__ __forceinline__ uint4 philox_quad(uint32_t q, const PhiloxStep& s, co
     return make_uint4(c0, c1, c2, c3);
 }
 
-// The parts of rounds 1-2 of philox_quad that depend only on (q, key, t_hi):
-// {hi(M1 c2r1) ^ k[2], lo(M1 c2r1), lo(M0 q) ^ k[3]}, c2r1 = hi(M0 q) ^ t_hi ^ k[1]
-// -- a per-quad table for the whole of a launch's steps with that t_hi
-__device__ __forceinline__ uint4 philox_quad_consts(uint32_t q, uint32_t t_hi, const uint32_t* __restrict__ rk)
-{
-    uint32_t lo0, hi0, lo1, hi1;
-    mulhilo(q, 0xD2511F53u, lo0, hi0);
-    mulhilo(hi0 ^ t_hi ^ rk[1], 0xCD9E8D57u, lo1, hi1);
-    return make_uint4(hi1 ^ rk[2], lo1, lo0 ^ rk[3], 0u);
-}
-
-// philox_quad with rounds 1-2's per-quad part taken from the table (two
-// 64-bit multiplies fewer per call): bit-identical output
-__device__ __forceinline__ uint4 philox_quad_pc(const uint4 pq, const PhiloxStep& s, const uint32_t* __restrict__ rk)
-{
-    uint32_t c0 = pq.x ^ s.c1r1;
-    uint32_t c1 = pq.y;
-    uint32_t c2 = s.hi0r2 ^ pq.z;
-    uint32_t c3 = s.lo0r2;
-#pragma unroll
-    for (int r = 2; r < 10; ++r) {
-        uint32_t a0, b0, a1, b1;
-        mulhilo(c0, 0xD2511F53u, a0, b0);
-        mulhilo(c2, 0xCD9E8D57u, a1, b1);
-        const uint32_t n0 = b1 ^ c1 ^ rk[2 * r];
-        const uint32_t n2 = b0 ^ c3 ^ rk[2 * r + 1];
-        c1 = a1;
-        c3 = a0;
-        c0 = n0;
-        c2 = n2;
-    }
-    return make_uint4(c0, c1, c2, c3);
-}
-
 // The lane-uniform part of rounds 1-3 of philox_quad for quad q at one step:
 // entering round 3, word 0 (hi(M1 c2r1) ^ lo(M1 t_lo) ^ k[2]) depends only on
 // (q, key, t), so its product with M0 is the same for every chain.  One lane
