@@ -103,7 +103,7 @@ def test_launch_shapes_equal_K1(pbn, per_node):
     pm = pbn.pbn_load(model, per_node=per_node)
     kw = dict(n_chains=200, steps=700, burn_in=300, seed=9, batch=64)
     ref = gpu_run(pm, model, pred, cluster_size=1, schedule=1, **kw)
-    for warps in [0, 1, 2, 5, 7, 8, 13, 24]:  # (24 = K1b's warp budget)
+    for warps in [0, 1, 2, 5, 7, 8, 13, 20, 21, 24]:  # (<= 20: the 640-thread build; 24 = K1b's warp budget)
         g = gpu_run(pm, model, pred, warps=warps, schedule=1, layout=BS, **kw)
         for k in ALL:
             assert np.array_equal(g[k], ref[k]), (warps, k)
